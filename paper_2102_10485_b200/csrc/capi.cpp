@@ -1,0 +1,477 @@
+// extern "C" surface: include/pg_kernels.h and include/pg_trainer.h.
+#include <cstring>
+#include <string>
+
+#include "../../include/pg_trainer.h"
+#include "gan.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F f) {
+  try {
+    f();
+    return PG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return PG_EINVAL;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return PG_EINVAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PG_ECUDA;
+  }
+}
+
+void cuda_ok(cudaError_t e, const char* what) { pg::check_cuda(e, what); }
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+pg::ConvGeo conv_geo(const pg_conv_desc* d) {
+  pg::ConvGeo g;
+  g.B = d->B;
+  g.GH = d->H;
+  g.GW = d->W;
+  g.CG = static_cast<int>(pg::pad4(d->Cin));
+  g.SH = d->OH;
+  g.SW = d->OW;
+  g.CS = static_cast<int>(pg::pad4(d->Cout));
+  g.k = d->k;
+  g.s = d->s;
+  g.p = d->p;
+  return g;
+}
+pg::ConvGeo convT_geo(const pg_conv_desc* d) {
+  pg::ConvGeo g;
+  g.B = d->B;
+  g.SH = d->H;
+  g.SW = d->W;
+  g.CS = static_cast<int>(pg::pad4(d->Cin));
+  g.GH = d->OH;
+  g.GW = d->OW;
+  g.CG = static_cast<int>(pg::pad4(d->Cout));
+  g.k = d->k;
+  g.s = d->s;
+  g.p = d->p;
+  return g;
+}
+pg::ConvGeo dense_geo(int B, int in, int out) {
+  pg::ConvGeo g;
+  g.B = B;
+  g.SH = g.SW = g.GH = g.GW = 1;
+  g.k = g.s = 1;
+  g.p = 0;
+  g.CS = static_cast<int>(pg::pad4(out));
+  g.CG = static_cast<int>(pg::pad4(in));
+  return g;
+}
+
+void check_desc(const pg_conv_desc* d, bool transposed) {
+  if (!d || d->B < 1 || d->Cin < 1 || d->Cout < 1 || d->k < 1 || d->s < 1 || d->p < 0)
+    throw std::invalid_argument("invalid convolution descriptor");
+  long oh = transposed ? (d->H - 1L) * d->s - 2L * d->p + d->k : (d->H + 2L * d->p - d->k) / d->s + 1;
+  long ow = transposed ? (d->W - 1L) * d->s - 2L * d->p + d->k : (d->W + 2L * d->p - d->k) / d->s + 1;
+  if (oh != d->OH || ow != d->OW) throw std::invalid_argument("output extent does not match the geometry");
+}
+
+long long small_ls(const pg::ConvGeo& g) { return static_cast<long long>(g.B) * g.SH * g.SW * g.CS; }
+long long big_ls(const pg::ConvGeo& g) { return static_cast<long long>(g.B) * g.GH * g.GW * g.CG; }
+
+struct Group {
+  int device;
+  std::unique_ptr<pg::GanGroup> g;
+};
+
+Group* G(pg_group* p) { return reinterpret_cast<Group*>(p); }
+
+}  // namespace
+
+extern "C" {
+
+const char* pg_last_error(void) { return g_err.c_str(); }
+
+int pg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+long long pg_launch_count(void) { return pg::launch_count(); }
+
+int pg_kernel_timing(int on) {
+  return guard([&] { pg::gemm_timing_enable(on != 0); });
+}
+
+int pg_kernel_timing_read(double* ms) {
+  return guard([&] { *ms = pg::gemm_timing_read_ms(); });
+}
+
+// ---------------- Conv2d ----------------
+int pg_conv2d_fwd(const pg_conv_desc* d, int L, const float* x, const float* w, long long w_ls, const float* bias,
+                  long long bias_ls, int act, float slope, float* y, int math, void* stream) {
+  return guard([&] {
+    check_desc(d, false);
+    pg::GemmArgs a{};
+    a.kind = pg::GEMM_FPROP;
+    a.g = conv_geo(d);
+    a.L = L;
+    a.big = x;
+    a.big_ls = big_ls(a.g);
+    a.w = w;
+    a.w_ls = w_ls;
+    a.out = y;
+    a.out_ls = small_ls(a.g);
+    a.bias = bias;
+    a.bias_ls = bias_ls;
+    a.act = act;
+    a.slope = slope;
+    a.c_valid = d->Cout;
+    a.c_pad = a.g.CS;
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), "conv2d_fwd");
+  });
+}
+
+int pg_conv2d_bwd_data(const pg_conv_desc* d, int L, const float* gy, const float* w, long long w_ls, float* gx,
+                       int math, void* stream) {
+  return guard([&] {
+    check_desc(d, false);
+    pg::GemmArgs a{};
+    a.kind = pg::GEMM_DGRAD;
+    a.g = conv_geo(d);
+    a.L = L;
+    a.small = gy;
+    a.small_ls = small_ls(a.g);
+    a.w = w;
+    a.w_ls = w_ls;
+    a.out = gx;
+    a.out_ls = big_ls(a.g);
+    a.c_valid = d->Cin;
+    a.c_pad = a.g.CG;
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), "conv2d_bwd_data");
+  });
+}
+
+int pg_conv2d_bwd_filter(const pg_conv_desc* d, int L, const float* x, const float* gy, float* gw, long long gw_ls,
+                         int accumulate, int math, void* stream) {
+  return guard([&] {
+    check_desc(d, false);
+    pg::GemmArgs a{};
+    a.kind = pg::GEMM_WGRAD;
+    a.g = conv_geo(d);
+    a.L = L;
+    a.small = gy;
+    a.small_ls = small_ls(a.g);
+    a.big = x;
+    a.big_ls = big_ls(a.g);
+    a.out = gw;
+    a.out_ls = gw_ls;
+    a.accumulate = accumulate;
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), "conv2d_bwd_filter");
+  });
+}
+
+// ---------------- ConvTranspose2d ----------------
+int pg_convT2d_fwd(const pg_conv_desc* d, int L, const float* x, const float* w, long long w_ls, const float* bias,
+                   long long bias_ls, int act, float slope, float* y, int math, void* stream) {
+  return guard([&] {
+    check_desc(d, true);
+    pg::GemmArgs a{};
+    a.kind = pg::GEMM_DGRAD;
+    a.g = convT_geo(d);
+    a.L = L;
+    a.small = x;
+    a.small_ls = small_ls(a.g);
+    a.w = w;
+    a.w_ls = w_ls;
+    a.out = y;
+    a.out_ls = big_ls(a.g);
+    a.bias = bias;
+    a.bias_ls = bias_ls;
+    a.act = act;
+    a.slope = slope;
+    a.c_valid = d->Cout;
+    a.c_pad = a.g.CG;
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), "convT2d_fwd");
+  });
+}
+
+int pg_convT2d_bwd_data(const pg_conv_desc* d, int L, const float* gy, const float* w, long long w_ls, float* gx,
+                        int math, void* stream) {
+  return guard([&] {
+    check_desc(d, true);
+    pg::GemmArgs a{};
+    a.kind = pg::GEMM_FPROP;
+    a.g = convT_geo(d);
+    a.L = L;
+    a.big = gy;
+    a.big_ls = big_ls(a.g);
+    a.w = w;
+    a.w_ls = w_ls;
+    a.out = gx;
+    a.out_ls = small_ls(a.g);
+    a.c_valid = d->Cin;
+    a.c_pad = a.g.CS;
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), "convT2d_bwd_data");
+  });
+}
+
+int pg_convT2d_bwd_filter(const pg_conv_desc* d, int L, const float* x, const float* gy, float* gw, long long gw_ls,
+                          int accumulate, int math, void* stream) {
+  return guard([&] {
+    check_desc(d, true);
+    pg::GemmArgs a{};
+    a.kind = pg::GEMM_WGRAD;
+    a.g = convT_geo(d);
+    a.L = L;
+    a.small = x;
+    a.small_ls = small_ls(a.g);
+    a.big = gy;
+    a.big_ls = big_ls(a.g);
+    a.out = gw;
+    a.out_ls = gw_ls;
+    a.accumulate = accumulate;
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), "convT2d_bwd_filter");
+  });
+}
+
+// ---------------- Dense ----------------
+int pg_dense_fwd(int L, int B, int in, int out, const float* x, const float* w, long long w_ls, const float* bias,
+                 long long bias_ls, int act, float slope, float* y, int math, void* stream) {
+  return guard([&] {
+    pg::GemmArgs a{};
+    a.kind = pg::GEMM_FPROP;
+    a.g = dense_geo(B, in, out);
+    a.L = L;
+    a.big = x;
+    a.big_ls = big_ls(a.g);
+    a.w = w;
+    a.w_ls = w_ls;
+    a.out = y;
+    a.out_ls = small_ls(a.g);
+    a.bias = bias;
+    a.bias_ls = bias_ls;
+    a.act = act;
+    a.slope = slope;
+    a.c_valid = out;
+    a.c_pad = a.g.CS;
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), "dense_fwd");
+  });
+}
+
+int pg_dense_bwd_data(int L, int B, int in, int out, const float* gy, const float* w, long long w_ls, float* gx,
+                      int math, void* stream) {
+  return guard([&] {
+    pg::GemmArgs a{};
+    a.kind = pg::GEMM_DGRAD;
+    a.g = dense_geo(B, in, out);
+    a.L = L;
+    a.small = gy;
+    a.small_ls = small_ls(a.g);
+    a.w = w;
+    a.w_ls = w_ls;
+    a.out = gx;
+    a.out_ls = big_ls(a.g);
+    a.c_valid = in;
+    a.c_pad = a.g.CG;
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), "dense_bwd_data");
+  });
+}
+
+int pg_dense_bwd_filter(int L, int B, int in, int out, const float* x, const float* gy, float* gw, long long gw_ls,
+                        int accumulate, int math, void* stream) {
+  return guard([&] {
+    pg::GemmArgs a{};
+    a.kind = pg::GEMM_WGRAD;
+    a.g = dense_geo(B, in, out);
+    a.L = L;
+    a.small = gy;
+    a.small_ls = small_ls(a.g);
+    a.big = x;
+    a.big_ls = big_ls(a.g);
+    a.out = gw;
+    a.out_ls = gw_ls;
+    a.accumulate = accumulate;
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), "dense_bwd_filter");
+  });
+}
+
+// ---------------- BatchNorm ----------------
+size_t pg_bn_workspace_floats(int L, int R, int Cp) {
+  pg::ChannelMap cm{L, R, Cp, Cp, 0};
+  return pg::reduce_partial_floats(cm) + static_cast<size_t>(L) * Cp * 3;
+}
+
+int pg_bn_fwd(int L, int R, int C, int Cp, const float* x, const float* gamma_beta, long long gb_ls, float* running,
+              long long run_ls, float eps, float momentum, int train, int act, float slope, float* mean, float* istd,
+              float* y, float* ws, void* stream) {
+  return guard([&] {
+    if (Cp % 4 || C > Cp || C < 1) throw std::invalid_argument("bn: channel padding must be a multiple of 4");
+    pg::ChannelMap cm{L, R, Cp, C, static_cast<long long>(R) * Cp};
+    if (train) {
+      cuda_ok(pg::launch_channel_reduce(cm, pg::RED_SUM, x, nullptr, nullptr, nullptr, 0, 0.f, ws, S(stream)), "bn");
+      cuda_ok(pg::launch_bn_finalize_mean(cm, ws, mean, S(stream)), "bn");
+      cuda_ok(pg::launch_channel_reduce(cm, pg::RED_SQDEV, x, nullptr, nullptr, mean, 0, 0.f, ws, S(stream)), "bn");
+      cuda_ok(pg::launch_bn_finalize_var(cm, ws, mean, istd, running, run_ls, eps, momentum, running ? 1 : 0, S(stream)),
+              "bn");
+    } else {
+      cuda_ok(pg::launch_bn_eval_stats(cm, running, run_ls, eps, mean, istd, S(stream)), "bn");
+    }
+    cuda_ok(pg::launch_bn_apply(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y, S(stream)), "bn");
+  });
+}
+
+int pg_bn_bwd(int L, int R, int C, int Cp, const float* gy, const float* y, const float* x, const float* mean,
+              const float* istd, const float* gamma_beta, long long gb_ls, int act, float slope, float* gx,
+              float* dgamma_beta, long long dgb_ls, int accumulate, float* ws, void* stream) {
+  return guard([&] {
+    pg::ChannelMap cm{L, R, Cp, C, static_cast<long long>(R) * Cp};
+    float* coef = ws + pg::reduce_partial_floats(cm);
+    cuda_ok(pg::launch_channel_reduce(cm, pg::RED_BN_BWD, x, gy, y, mean, act, slope, ws, S(stream)), "bn bwd");
+    cuda_ok(pg::launch_bn_bwd_finalize(cm, ws, istd, gamma_beta, gb_ls, dgamma_beta, dgb_ls, nullptr, 0, accumulate, 1,
+                                       coef, S(stream)),
+            "bn bwd");
+    cuda_ok(pg::launch_bn_bwd_apply(cm, gy, y, x, mean, coef, act, slope, gx, S(stream)), "bn bwd");
+  });
+}
+
+int pg_act_bwd(long long n, const float* gy, const float* y, int act, float slope, float* gx, void* stream) {
+  return guard([&] {
+    if (n % 4) throw std::invalid_argument("act_bwd: n must be a multiple of 4");
+    pg::ChannelMap cm{1, static_cast<int>(n / 4), 4, 4, n};
+    cuda_ok(pg::launch_act_bwd(cm, gy, y, act, slope, gx, S(stream)), "act_bwd");
+  });
+}
+
+int pg_gan_losses(int L, int B, const float* p_real, const float* p_fake, int pstride, double clamp, float* g_real,
+                  float* g_fake, double* report, void* stream) {
+  return guard([&] {
+    if (!(clamp > 0 && clamp < 0.5)) throw std::invalid_argument("probability clamp must lie in (0, 0.5)");
+    if (B < 1 || B > 1024) throw std::invalid_argument("gan_losses: batch must be in [1, 1024]");
+    cuda_ok(pg::launch_loss_d(L, B, p_real, p_fake, pstride, clamp, g_real, g_fake, report, S(stream)), "loss");
+  });
+}
+
+int pg_gen_loss(int L, int B, const float* p_fake, int pstride, double clamp, float* g, double* report, void* stream) {
+  return guard([&] {
+    if (!(clamp > 0 && clamp < 0.5)) throw std::invalid_argument("probability clamp must lie in (0, 0.5)");
+    if (B < 1 || B > 1024) throw std::invalid_argument("gen_loss: batch must be in [1, 1024]");
+    cuda_ok(pg::launch_loss_g(L, B, p_fake, pstride, clamp, g, report, S(stream)), "loss");
+  });
+}
+
+int pg_adam_step(int L, long long P, float* params, const float* grads, float* m, float* v, long long* t, int* flags,
+                 float lr, float beta1, float beta2, float eps, void* stream) {
+  return guard([&] {
+    if (P % 4) throw std::invalid_argument("adam_step: arena length must be a multiple of 4");
+    cuda_ok(pg::launch_nonfinite_check(L, P, grads, flags, S(stream)), "adam");
+    cuda_ok(pg::launch_adam_tick(L, flags, t, S(stream)), "adam");
+    cuda_ok(pg::launch_adam(L, P, params, grads, m, v, t, flags, lr, beta1, beta2, eps, S(stream)), "adam");
+  });
+}
+
+int pg_gather_real(int L, int B, const int* idx, const float* data, long long data_ls, long long sample, int Cp, int C,
+                   float* out, void* stream) {
+  return guard([&] {
+    cuda_ok(pg::launch_gather_real(L, B, idx, data, data_ls, sample, Cp, C, out, S(stream)), "gather");
+  });
+}
+
+// ---------------- trainer ----------------
+int pg_group_create(const pg_group_config* c, pg_group** out) {
+  return guard([&] {
+    if (!c || !out) throw std::invalid_argument("null argument");
+    *out = nullptr;
+    cuda_ok(cudaSetDevice(c->device), "cudaSetDevice");
+    pg::GroupConfig cfg;
+    cfg.gen_spec = c->gen_spec ? c->gen_spec : "";
+    cfg.disc_spec = c->disc_spec ? c->disc_spec : "";
+    cfg.C = c->C;
+    cfg.H = c->H;
+    cfg.W = c->W;
+    cfg.d_z = c->d_z;
+    if (c->n_labels < 1 || !c->class_ids) throw std::invalid_argument("pg_group_create: no labels");
+    cfg.class_ids.assign(c->class_ids, c->class_ids + c->n_labels);
+    cfg.base_seed = c->base_seed;
+    cfg.batch = c->batch;
+    cfg.epochs = c->epochs;
+    cfg.per_label = c->per_label;
+    cfg.lr = c->lr;
+    cfg.beta1 = c->beta1;
+    cfg.beta2 = c->beta2;
+    cfg.eps = c->eps;
+    cfg.clamp = c->clamp;
+    cfg.init_std = c->init_std;
+    cfg.math = c->math;
+    cfg.threads = c->threads;
+    auto grp = std::make_unique<Group>();
+    grp->device = c->device;
+    grp->g = std::make_unique<pg::GanGroup>(cfg);
+    *out = reinterpret_cast<pg_group*>(grp.release());
+  });
+}
+
+void pg_group_destroy(pg_group* g) {
+  if (!g) return;
+  cudaSetDevice(G(g)->device);
+  delete G(g);
+}
+
+#define WITH_GROUP(body)                                    \
+  guard([&] {                                               \
+    if (!g) throw std::invalid_argument("null group");      \
+    cuda_ok(cudaSetDevice(G(g)->device), "cudaSetDevice");  \
+    pg::GanGroup& grp = *G(g)->g;                           \
+    (void)grp;                                              \
+    body;                                                   \
+  })
+
+int pg_group_set_dataset(pg_group* g, const float* images01) { return WITH_GROUP(grp.set_dataset(images01)); }
+int pg_group_generate_dataset(pg_group* g, uint64_t seed) { return WITH_GROUP(grp.generate_dataset(seed)); }
+int pg_group_train_steps(pg_group* g, int n) {
+  int done = 0;
+  int rc = WITH_GROUP(done = grp.train_steps(n));
+  return rc == PG_OK ? done : rc;
+}
+int pg_group_train_step(pg_group* g, const float* real01, int B, double* reports) {
+  return WITH_GROUP(grp.train_step_host(real01, B, reports));
+}
+int pg_group_train_step_inputs(pg_group* g, const float* real01, const float* z1, const float* z2, int B,
+                               double* reports) {
+  return WITH_GROUP(grp.train_step_inputs(real01, z1, z2, B, reports));
+}
+long pg_group_get(pg_group* g, int label, int field, double* out, long cap) {
+  long n = -1;
+  int rc = WITH_GROUP(n = grp.get(label, field, out, cap));
+  return rc == PG_OK ? n : rc;
+}
+int pg_group_set(pg_group* g, int label, int field, const double* in, long n) {
+  return WITH_GROUP(grp.set(label, field, in, n));
+}
+int pg_group_failed(pg_group* g, int* failed) {
+  return WITH_GROUP({
+    auto f = grp.failed();
+    std::memcpy(failed, f.data(), f.size() * sizeof(int));
+  });
+}
+int pg_group_generate(pg_group* g, long n, uint64_t seed, float* out) { return WITH_GROUP(grp.generate(n, seed, out)); }
+float pg_group_last_ms(pg_group* g) { return g ? G(g)->g->last_device_ms() : -1.f; }
+int pg_group_sync(pg_group* g) { return WITH_GROUP(grp.sync()); }
+int pg_group_sizes(pg_group* g, long long* out) {
+  return WITH_GROUP({
+    out[0] = grp.gen().ref_params();
+    out[1] = grp.disc().ref_params();
+    out[2] = grp.gen().P();
+    out[3] = grp.disc().P();
+  });
+}
+
+uint64_t pg_derive_seed(uint64_t base, uint64_t stream) { return pg::derive_seed(base, stream); }
+int pg_shard_begin(int n_labels, int n_gpus, int g) { return pg::shard_begin(n_labels, n_gpus, g); }
+int pg_cosine_label(int C, int H, int W, long per_label, uint64_t seed, int label, double* out) {
+  return guard([&] { pg::cosine_label(C, H, W, per_label, seed, label, out); });
+}
+
+}  // extern "C"

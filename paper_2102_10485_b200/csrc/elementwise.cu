@@ -1,0 +1,528 @@
+// HBM-bound kernels of the training step, all batched over the L labels of a
+// GPU: per-channel reductions (BatchNorm statistics and backward sums, bias
+// gradients), BatchNorm apply with the fused activation, the fused
+// activation/BatchNorm backward, the GAN losses, Adam, and data movement.
+// Reductions are deterministic: fixed row chunks, fixed in-block order and a
+// fixed-order second pass over the chunk partials (no float atomics).
+#include "kernels.hpp"
+
+#include <cmath>
+
+namespace pg {
+
+namespace {
+
+constexpr int RED_ROWS = 128;  // rows per reduction chunk
+constexpr int RED_TY = 8;      // row lanes per block (block = 32 channels x 8)
+
+__global__ void channel_reduce_kernel(ChannelMap cm, int mode, const float* __restrict__ x,
+                                      const float* __restrict__ gy, const float* __restrict__ y,
+                                      const float* __restrict__ mean, int act, float slope,
+                                      float* __restrict__ partial) {
+  const int l = blockIdx.z, chunk = blockIdx.x;
+  const int c = blockIdx.y * 32 + threadIdx.x;
+  const int nchunk = gridDim.x;
+  const long long base = (long long)l * cm.ls;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+  if (c < cm.Cp) {
+    const float mu = (mode == RED_SQDEV || mode == RED_BN_BWD) ? mean[(long long)l * cm.Cp + c] : 0.f;
+    const int r_end = min(cm.R, (chunk + 1) * RED_ROWS);
+    for (int r = chunk * RED_ROWS + threadIdx.y; r < r_end; r += RED_TY) {
+      const long long o = base + (long long)r * cm.Cp + c;
+      switch (mode) {
+        case RED_SUM: s0 += x[o]; break;
+        case RED_SQDEV: {
+          float d = x[o] - mu;
+          s0 += d * d;
+          break;
+        }
+        case RED_BN_BWD: {
+          float g1 = act_bwd(act, gy[o], y[o], slope);
+          float d = x[o] - mu;
+          s0 += g1;
+          s1 += g1 * d;
+          s2 += d;
+          break;
+        }
+        default: s0 += act_bwd(act, gy[o], y[o], slope); break;
+      }
+    }
+  }
+  __shared__ float sm[3][RED_TY][33];
+  sm[0][threadIdx.y][threadIdx.x] = s0;
+  sm[1][threadIdx.y][threadIdx.x] = s1;
+  sm[2][threadIdx.y][threadIdx.x] = s2;
+  __syncthreads();
+  if (threadIdx.y < 3 && c < cm.Cp) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < RED_TY; ++i) t += sm[threadIdx.y][i][threadIdx.x];
+    partial[(((long long)l * nchunk + chunk) * 3 + threadIdx.y) * cm.Cp + c] = t;
+  }
+}
+
+PG_DEV float sum_partials(const ChannelMap& cm, const float* partial, int l, int k, int c) {
+  const int nchunk = (cm.R + RED_ROWS - 1) / RED_ROWS;
+  float t = 0.f;
+  for (int ch = 0; ch < nchunk; ++ch) t += partial[(((long long)l * nchunk + ch) * 3 + k) * cm.Cp + c];
+  return t;
+}
+
+__global__ void bn_finalize_mean_kernel(ChannelMap cm, const float* partial, float* mean) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cm.L * cm.Cp) return;
+  int l = i / cm.Cp, c = i % cm.Cp;
+  mean[i] = sum_partials(cm, partial, l, 0, c) / (float)cm.R;
+}
+
+__global__ void bn_finalize_var_kernel(ChannelMap cm, const float* partial, const float* mean, float* istd,
+                                       float* running, long long run_ls, float eps, float mom, int update) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cm.L * cm.Cp) return;
+  int l = i / cm.Cp, c = i % cm.Cp;
+  const float m = (float)cm.R;
+  float var = sum_partials(cm, partial, l, 0, c) / m;
+  istd[i] = 1.f / sqrtf(var + eps);
+  if (update && c < cm.C) {
+    // running buffers: [mean[C]][var[C]] per label (reference buffer layout)
+    float* rm = running + (long long)l * run_ls;
+    float* rv = rm + cm.C;
+    float unbias = m > 1.f ? m / (m - 1.f) : 1.f;
+    rm[c] = (1.f - mom) * rm[c] + mom * mean[i];
+    rv[c] = (1.f - mom) * rv[c] + mom * var * unbias;
+  }
+}
+
+__global__ void bn_eval_stats_kernel(ChannelMap cm, const float* running, long long run_ls, float eps, float* mean,
+                                     float* istd) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cm.L * cm.Cp) return;
+  int l = i / cm.Cp, c = i % cm.Cp;
+  if (c < cm.C) {
+    const float* rm = running + (long long)l * run_ls;
+    mean[i] = rm[c];
+    istd[i] = 1.f / sqrtf(rm[cm.C + c] + eps);
+  } else {
+    mean[i] = 0.f;
+    istd[i] = 0.f;
+  }
+}
+
+// float4 over [L][R][Cp] (Cp % 4 == 0)
+__global__ void bn_apply_kernel(ChannelMap cm, const float* __restrict__ x, const float* __restrict__ mean,
+                                const float* __restrict__ istd, const float* __restrict__ gb, long long gb_ls, int act,
+                                float slope, float* __restrict__ y) {
+  const long long per = (long long)cm.R * cm.Cp / 4;
+  const int l = blockIdx.y;
+  const float* gamma = gb + (long long)l * gb_ls;
+  const float* beta = gamma + cm.C;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < per; q += (long long)gridDim.x * blockDim.x) {
+    const long long o = (long long)l * cm.ls + q * 4;
+    const int c0 = (int)((q * 4) % cm.Cp);
+    float4 v = *reinterpret_cast<const float4*>(x + o);
+    float r[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int c = c0 + u;
+      if (c < cm.C) {
+        long long mc = (long long)l * cm.Cp + c;
+        r[u] = act_fwd(act, gamma[c] * ((r[u] - mean[mc]) * istd[mc]) + beta[c], slope);
+      } else {
+        r[u] = 0.f;
+      }
+    }
+    *reinterpret_cast<float4*>(y + o) = make_float4(r[0], r[1], r[2], r[3]);
+  }
+}
+
+// coef[l][c][3] = {gamma*istd, 2*dvar/m, dmean/m}
+__global__ void bn_bwd_finalize_kernel(ChannelMap cm, const float* partial, const float* istd, const float* gb,
+                                       long long gb_ls, float* dgb, long long dgb_ls, float* dbias, long long dbias_ls,
+                                       int accumulate, int train, float* coef) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cm.L * cm.Cp) return;
+  int l = i / cm.Cp, c = i % cm.Cp;
+  float* cf = coef + (long long)i * 3;
+  if (c >= cm.C) {
+    cf[0] = cf[1] = cf[2] = 0.f;
+    return;
+  }
+  const float m = (float)cm.R;
+  const float S1 = sum_partials(cm, partial, l, 0, c);
+  const float S2 = sum_partials(cm, partial, l, 1, c);
+  const float S3 = sum_partials(cm, partial, l, 2, c);
+  const float is = istd[i];
+  const float gamma = gb[(long long)l * gb_ls + c];
+  float dg = S2 * is, db = S1;
+  float a = gamma * is, dvar = 0.f, dmean = 0.f;
+  if (train) {
+    dvar = gamma * S2 * (-0.5f) * is * is * is;
+    dmean = -gamma * S1 * is + dvar * (-2.f / m) * S3;
+  }
+  cf[0] = a;
+  cf[1] = 2.f * dvar / m;
+  cf[2] = dmean / m;
+  float* dgp = dgb + (long long)l * dgb_ls;
+  if (accumulate) {
+    dgp[c] += dg;
+    dgp[cm.C + c] += db;
+  } else {
+    dgp[c] = dg;
+    dgp[cm.C + c] = db;
+  }
+  if (dbias) {
+    // sum over rows of gz, in closed form from the channel sums
+    float sgz = a * S1 + cf[1] * S3 + dmean;
+    float* d = dbias + (long long)l * dbias_ls + c;
+    *d = accumulate ? *d + sgz : sgz;
+  }
+}
+
+__global__ void bn_bwd_apply_kernel(ChannelMap cm, const float* __restrict__ gy, const float* __restrict__ y,
+                                    const float* __restrict__ x, const float* __restrict__ mean,
+                                    const float* __restrict__ coef, int act, float slope, float* __restrict__ gz) {
+  const long long per = (long long)cm.R * cm.Cp / 4;
+  const int l = blockIdx.y;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < per; q += (long long)gridDim.x * blockDim.x) {
+    const long long o = (long long)l * cm.ls + q * 4;
+    const int c0 = (int)((q * 4) % cm.Cp);
+    float4 g4 = *reinterpret_cast<const float4*>(gy + o);
+    float4 y4 = *reinterpret_cast<const float4*>(y + o);
+    float4 x4 = *reinterpret_cast<const float4*>(x + o);
+    float g[4] = {g4.x, g4.y, g4.z, g4.w}, yy[4] = {y4.x, y4.y, y4.z, y4.w}, xx[4] = {x4.x, x4.y, x4.z, x4.w};
+    float r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      long long mc = (long long)l * cm.Cp + c0 + u;
+      const float* cf = coef + mc * 3;
+      float g1 = act_bwd(act, g[u], yy[u], slope);
+      r[u] = g1 * cf[0] + cf[1] * (xx[u] - mean[mc]) + cf[2];
+    }
+    *reinterpret_cast<float4*>(gz + o) = make_float4(r[0], r[1], r[2], r[3]);
+  }
+}
+
+__global__ void act_bwd_kernel(ChannelMap cm, const float* __restrict__ gy, const float* __restrict__ y, int act,
+                               float slope, float* g) {
+  const long long per = (long long)cm.R * cm.Cp / 4;
+  const int l = blockIdx.y;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < per; q += (long long)gridDim.x * blockDim.x) {
+    const long long o = (long long)l * cm.ls + q * 4;
+    float4 g4 = *reinterpret_cast<const float4*>(gy + o);
+    float4 y4 = *reinterpret_cast<const float4*>(y + o);
+    float4 r = make_float4(act_bwd(act, g4.x, y4.x, slope), act_bwd(act, g4.y, y4.y, slope),
+                           act_bwd(act, g4.z, y4.z, slope), act_bwd(act, g4.w, y4.w, slope));
+    *reinterpret_cast<float4*>(g + o) = r;
+  }
+}
+
+__global__ void bias_finalize_kernel(ChannelMap cm, const float* partial, float* dbias, long long dbias_ls,
+                                     int accumulate) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cm.L * cm.C) return;
+  int l = i / cm.C, c = i % cm.C;
+  float s = sum_partials(cm, partial, l, 0, c);
+  float* d = dbias + (long long)l * dbias_ls + c;
+  *d = accumulate ? *d + s : s;
+}
+
+// ---- losses: one block per label, fixed-order tree in double ----
+__device__ double block_sum(double v, double* sm) {
+  const int t = threadIdx.x;
+  sm[t] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (t < w) sm[t] += sm[t + w];
+    __syncthreads();
+  }
+  double r = sm[0];
+  __syncthreads();
+  return r;
+}
+
+PG_DEV double clampd(double p, double c) { return fmin(fmax(p, c), 1.0 - c); }
+PG_DEV bool inside(double p, double c) { return p > c && p < 1.0 - c; }
+
+__global__ void loss_d_kernel(int B, const float* pr, const float* pf, int ps, double clamp, float* gr, float* gf,
+                              double* rep) {
+  extern __shared__ double sm[];
+  const int l = blockIdx.x, i = threadIdx.x;
+  double lr = 0, lf = 0, mr = 0, mf = 0;
+  if (i < B) {
+    long long o = ((long long)l * B + i) * ps;
+    double a = pr[o], b = pf[o];
+    lr = log(clampd(a, clamp));
+    lf = log(1.0 - clampd(b, clamp));
+    mr = a;
+    mf = b;
+    gr[o] = inside(a, clamp) ? (float)(-0.5 / ((double)B * a)) : 0.f;
+    gf[o] = inside(b, clamp) ? (float)(0.5 / ((double)B * (1.0 - b))) : 0.f;
+    for (int c = 1; c < ps; ++c) gr[o + c] = gf[o + c] = 0.f;
+  }
+  double slr = block_sum(lr, sm), slf = block_sum(lf, sm), smr = block_sum(mr, sm), smf = block_sum(mf, sm);
+  if (i == 0) {
+    rep[l * 4 + 0] = -0.5 * slr / B - 0.5 * slf / B;
+    rep[l * 4 + 2] = smr / B;
+    rep[l * 4 + 3] = smf / B;
+  }
+}
+
+__global__ void loss_g_kernel(int B, const float* pf, int ps, double clamp, float* g, double* rep) {
+  extern __shared__ double sm[];
+  const int l = blockIdx.x, i = threadIdx.x;
+  double lg = 0;
+  if (i < B) {
+    long long o = ((long long)l * B + i) * ps;
+    double b = pf[o];
+    lg = log(clampd(b, clamp));
+    g[o] = inside(b, clamp) ? (float)(-0.5 / ((double)B * b)) : 0.f;
+    for (int c = 1; c < ps; ++c) g[o + c] = 0.f;
+  }
+  double s = block_sum(lg, sm);
+  if (i == 0) rep[l * 4 + 1] = 0.5 * s / B;
+}
+
+// ---- Adam ----
+__global__ void nonfinite_kernel(long long P, const float* __restrict__ g, int* flags) {
+  const int l = blockIdx.y;
+  const float* gl = g + (long long)l * P;
+  bool bad = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P / 4; i += (long long)gridDim.x * blockDim.x) {
+    float4 v = reinterpret_cast<const float4*>(gl)[i];
+    bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags + l, 1);
+}
+
+__global__ void adam_tick_kernel(int L, const int* flags, long long* t) {
+  int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < L && !flags[l]) t[l] += 1;
+}
+
+__global__ void adam_kernel(long long P, float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, const long long* t, const int* flags, float lr, float b1, float b2,
+                            float eps) {
+  const int l = blockIdx.y;
+  if (flags[l]) return;  // rejected step: state untouched (optim.cpp:25)
+  __shared__ float c12[2];
+  if (threadIdx.x == 0) {
+    double tt = (double)t[l];
+    c12[0] = (float)(1.0 - pow((double)b1, tt));
+    c12[1] = (float)(1.0 - pow((double)b2, tt));
+  }
+  __syncthreads();
+  const float c1 = c12[0], c2 = c12[1];
+  const long long off = (long long)l * P;
+  float4* p4 = reinterpret_cast<float4*>(p + off);
+  const float4* g4 = reinterpret_cast<const float4*>(g + off);
+  float4* m4 = reinterpret_cast<float4*>(m + off);
+  float4* v4 = reinterpret_cast<float4*>(v + off);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P / 4; i += (long long)gridDim.x * blockDim.x) {
+    float4 gg = g4[i], mm = m4[i], vv = v4[i], pp = p4[i];
+    float ga[4] = {gg.x, gg.y, gg.z, gg.w}, ma[4] = {mm.x, mm.y, mm.z, mm.w}, va[4] = {vv.x, vv.y, vv.z, vv.w},
+          pa[4] = {pp.x, pp.y, pp.z, pp.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      ma[u] = b1 * ma[u] + (1.f - b1) * ga[u];
+      va[u] = b2 * va[u] + (1.f - b2) * ga[u] * ga[u];
+      pa[u] -= lr * (ma[u] / c1) / (sqrtf(va[u] / c2) + eps);
+    }
+    m4[i] = make_float4(ma[0], ma[1], ma[2], ma[3]);
+    v4[i] = make_float4(va[0], va[1], va[2], va[3]);
+    p4[i] = make_float4(pa[0], pa[1], pa[2], pa[3]);
+  }
+}
+
+// ---- data movement ----
+__global__ void gather_real_kernel(int B, const int* __restrict__ idx, const float* __restrict__ data,
+                                   long long data_ls, long long sample, int Cp, int C, float* __restrict__ out) {
+  const int l = blockIdx.z, b = blockIdx.y;
+  const long long src = (long long)l * data_ls + (long long)idx[l * B + b] * sample;
+  const long long dst = ((long long)l * B + b) * sample;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < sample / 4;
+       q += (long long)gridDim.x * blockDim.x) {
+    float4 v = reinterpret_cast<const float4*>(data + src)[q];
+    int c0 = (int)((q * 4) % Cp);
+    float r[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = (c0 + u < C) ? r[u] * 2.f - 1.f : 0.f;
+    reinterpret_cast<float4*>(out + dst)[q] = make_float4(r[0], r[1], r[2], r[3]);
+  }
+}
+
+__global__ void nchw01_to_nhwc_kernel(long long N, int C, int H, int W, int Cp, const float* in, float* out, int map) {
+  long long total = N * H * W * Cp;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(i % Cp);
+    long long pix = i / Cp;
+    int x = (int)(pix % W);
+    long long t = pix / W;
+    int y = (int)(t % H);
+    long long n = t / H;
+    float v = c < C ? in[((n * C + c) * H + y) * W + x] : 0.f;
+    out[i] = (map && c < C) ? v * 2.f - 1.f : v;
+  }
+}
+
+__global__ void nhwc_to_nchw01_kernel(long long N, int C, int H, int W, int Cp, const float* in, float* out) {
+  long long total = N * C * H * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    int x = (int)(i % W);
+    long long t = i / W;
+    int y = (int)(t % H);
+    t /= H;
+    int c = (int)(t % C);
+    long long n = t / C;
+    out[i] = (in[((n * H + y) * W + x) * Cp + c] + 1.f) * 0.5f;
+  }
+}
+
+__global__ void fill_kernel(float* p, long long n, float v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+unsigned grid_for(long long work, int per_block, unsigned cap = 148 * 16) {
+  long long g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+}  // namespace
+
+int reduce_chunks(int R) { return (R + RED_ROWS - 1) / RED_ROWS; }
+size_t reduce_partial_floats(const ChannelMap& cm) { return (size_t)cm.L * reduce_chunks(cm.R) * 3 * cm.Cp; }
+
+cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x, const float* gy, const float* y,
+                                  const float* mean, int act, float slope, float* partial, cudaStream_t st) {
+  dim3 grid(reduce_chunks(cm.R), (cm.Cp + 31) / 32, cm.L);
+  channel_reduce_kernel<<<grid, dim3(32, RED_TY), 0, st>>>(cm, mode, x, gy, y, mean, act, slope, partial);
+  return launched();
+}
+
+cudaError_t launch_bn_finalize_mean(const ChannelMap& cm, const float* partial, float* mean, cudaStream_t st) {
+  int n = cm.L * cm.Cp;
+  bn_finalize_mean_kernel<<<(n + 255) / 256, 256, 0, st>>>(cm, partial, mean);
+  return launched();
+}
+
+cudaError_t launch_bn_finalize_var(const ChannelMap& cm, const float* partial, const float* mean, float* istd,
+                                   float* running, long long run_ls, float eps, float momentum, int update_running,
+                                   cudaStream_t st) {
+  int n = cm.L * cm.Cp;
+  bn_finalize_var_kernel<<<(n + 255) / 256, 256, 0, st>>>(cm, partial, mean, istd, running, run_ls, eps, momentum,
+                                                          update_running);
+  return launched();
+}
+
+cudaError_t launch_bn_eval_stats(const ChannelMap& cm, const float* running, long long run_ls, float eps, float* mean,
+                                 float* istd, cudaStream_t st) {
+  int n = cm.L * cm.Cp;
+  bn_eval_stats_kernel<<<(n + 255) / 256, 256, 0, st>>>(cm, running, run_ls, eps, mean, istd);
+  return launched();
+}
+
+cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* mean, const float* istd,
+                            const float* gamma_beta, long long gb_ls, int act, float slope, float* y, cudaStream_t st) {
+  dim3 grid(grid_for((long long)cm.R * cm.Cp / 4, 256, 4096), cm.L);
+  bn_apply_kernel<<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y);
+  return launched();
+}
+
+cudaError_t launch_bn_bwd_finalize(const ChannelMap& cm, const float* partial, const float* istd,
+                                   const float* gamma_beta, long long gb_ls, float* dgamma_beta, long long dgb_ls,
+                                   float* dbias, long long dbias_ls, int accumulate, int train, float* coef,
+                                   cudaStream_t st) {
+  int n = cm.L * cm.Cp;
+  bn_bwd_finalize_kernel<<<(n + 255) / 256, 256, 0, st>>>(cm, partial, istd, gamma_beta, gb_ls, dgamma_beta, dgb_ls,
+                                                          dbias, dbias_ls, accumulate, train, coef);
+  return launched();
+}
+
+cudaError_t launch_bn_bwd_apply(const ChannelMap& cm, const float* gy, const float* y, const float* x,
+                                const float* mean, const float* coef, int act, float slope, float* gz,
+                                cudaStream_t st) {
+  dim3 grid(grid_for((long long)cm.R * cm.Cp / 4, 256, 4096), cm.L);
+  bn_bwd_apply_kernel<<<grid, 256, 0, st>>>(cm, gy, y, x, mean, coef, act, slope, gz);
+  return launched();
+}
+
+cudaError_t launch_act_bwd(const ChannelMap& cm, const float* gy, const float* y, int act, float slope, float* g,
+                           cudaStream_t st) {
+  dim3 grid(grid_for((long long)cm.R * cm.Cp / 4, 256, 4096), cm.L);
+  act_bwd_kernel<<<grid, 256, 0, st>>>(cm, gy, y, act, slope, g);
+  return launched();
+}
+
+cudaError_t launch_bias_finalize(const ChannelMap& cm, const float* partial, float* dbias, long long dbias_ls,
+                                 int accumulate, cudaStream_t st) {
+  int n = cm.L * cm.C;
+  bias_finalize_kernel<<<(n + 255) / 256, 256, 0, st>>>(cm, partial, dbias, dbias_ls, accumulate);
+  return launched();
+}
+
+static int pow2_at_least(int b) {
+  int t = 32;
+  while (t < b) t <<= 1;
+  return t;
+}
+
+cudaError_t launch_loss_d(int L, int B, const float* p_real, const float* p_fake, int pstride, double clamp,
+                          float* g_real, float* g_fake, double* report, cudaStream_t st) {
+  int t = pow2_at_least(B);
+  loss_d_kernel<<<L, t, t * sizeof(double), st>>>(B, p_real, p_fake, pstride, clamp, g_real, g_fake, report);
+  return launched();
+}
+
+cudaError_t launch_loss_g(int L, int B, const float* p_fake, int pstride, double clamp, float* g, double* report,
+                          cudaStream_t st) {
+  int t = pow2_at_least(B);
+  loss_g_kernel<<<L, t, t * sizeof(double), st>>>(B, p_fake, pstride, clamp, g, report);
+  return launched();
+}
+
+cudaError_t launch_nonfinite_check(int L, long long P, const float* grads, int* flags, cudaStream_t st) {
+  dim3 grid(grid_for(P / 4, 256, 64), L);
+  nonfinite_kernel<<<grid, 256, 0, st>>>(P, grads, flags);
+  return launched();
+}
+
+cudaError_t launch_adam_tick(int L, const int* flags, long long* t, cudaStream_t st) {
+  adam_tick_kernel<<<(L + 127) / 128, 128, 0, st>>>(L, flags, t);
+  return launched();
+}
+
+cudaError_t launch_adam(int L, long long P, float* params, const float* grads, float* m, float* v,
+                        const long long* t, const int* flags, float lr, float b1, float b2, float eps,
+                        cudaStream_t st) {
+  dim3 grid(grid_for(P / 4, 256, 256), L);
+  adam_kernel<<<grid, 256, 0, st>>>(P, params, grads, m, v, t, flags, lr, b1, b2, eps);
+  return launched();
+}
+
+cudaError_t launch_gather_real(int L, int B, const int* idx, const float* data, long long data_ls, long long sample,
+                               int Cp, int C, float* out, cudaStream_t st) {
+  dim3 grid(grid_for(sample / 4, 256, 16), B, L);
+  gather_real_kernel<<<grid, 256, 0, st>>>(B, idx, data, data_ls, sample, Cp, C, out);
+  return launched();
+}
+
+cudaError_t launch_nchw01_to_nhwc(long long N, int C, int H, int W, int Cp, const float* in, float* out,
+                                  cudaStream_t st, int map2x1) {
+  nchw01_to_nhwc_kernel<<<grid_for(N * H * W * Cp, 256, 148 * 8), 256, 0, st>>>(N, C, H, W, Cp, in, out, map2x1);
+  return launched();
+}
+
+cudaError_t launch_nhwc_to_nchw01(long long N, int C, int H, int W, int Cp, const float* in, float* out,
+                                  cudaStream_t st) {
+  nhwc_to_nchw01_kernel<<<grid_for(N * C * H * W, 256, 148 * 8), 256, 0, st>>>(N, C, H, W, Cp, in, out);
+  return launched();
+}
+
+cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t st) {
+  fill_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(p, n, v);
+  return launched();
+}
+
+}  // namespace pg

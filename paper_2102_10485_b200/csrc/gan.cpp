@@ -1,0 +1,478 @@
+#include "gan.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace pg {
+
+namespace {
+template <class T>
+T* pinned(size_t n) {
+  void* p = nullptr;
+  check_cuda(cudaMallocHost(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMallocHost");
+  std::memset(p, 0, std::max<size_t>(n, 1) * sizeof(T));
+  return static_cast<T*>(p);
+}
+template <class T>
+T* dev_alloc(size_t n) {
+  void* p = nullptr;
+  check_cuda(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+  check_cuda(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)), "cudaMemset");
+  return static_cast<T*>(p);
+}
+std::string shape3(long C, long H, long W) {
+  return std::to_string(C) + " " + std::to_string(H) + " " + std::to_string(W);
+}
+}  // namespace
+
+GanGroup::GanGroup(const GroupConfig& cfg) : cfg_(cfg), L_(static_cast<int>(cfg.class_ids.size())) {
+  if (L_ < 1) throw std::invalid_argument("GanGroup: no labels");
+  if (cfg_.batch < 1) throw std::invalid_argument("GanGroup: batch size must be positive");
+  if (cfg_.per_label < 1) throw std::invalid_argument("GanGroup: empty shard");
+  if (!(cfg_.clamp > 0.0 && cfg_.clamp < 0.5))
+    throw std::invalid_argument("probability clamp must lie in (0, 0.5), got " + std::to_string(cfg_.clamp));
+  if (cfg_.d_z < 1) throw std::invalid_argument("latent dimension must be positive");
+  const int Bmax = static_cast<int>(std::min<long>(cfg_.batch, cfg_.per_label));
+  G_ = std::make_unique<DevNet>(cfg_.gen_spec, std::vector<long>{cfg_.d_z}, L_, Bmax, cfg_.math);
+  D_ = std::make_unique<DevNet>(cfg_.disc_spec, std::vector<long>{cfg_.C, cfg_.H, cfg_.W}, L_, Bmax, cfg_.math);
+  // make_gan_pair shape checks (gan.cpp:41-48)
+  std::vector<long> img{cfg_.C, cfg_.H, cfg_.W};
+  if (G_->ref_out_shape() != img)
+    throw std::invalid_argument("generator emits a shape that does not match images " + shape3(cfg_.C, cfg_.H, cfg_.W));
+  long dout = 1;
+  for (long d : D_->ref_out_shape()) dout *= d;
+  if (dout != 1) throw std::invalid_argument("discriminator must emit a scalar");
+
+  check_cuda(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+  tg_ = G_->make_trace(true);
+  tdr_ = D_->make_trace(true);
+  tdf_ = D_->make_trace(true);
+  zcp_ = pad4(cfg_.d_z);
+  const Map& im = D_->in_map();
+  data_ = DeviceBuf(static_cast<size_t>(L_) * cfg_.per_label * im.numel());
+  real_ = DeviceBuf(static_cast<size_t>(L_) * Bmax * im.numel());
+  gimg_ = DeviceBuf(static_cast<size_t>(L_) * Bmax * im.numel());
+  const long pout = D_->out_map().Cp;
+  gp_real_ = DeviceBuf(static_cast<size_t>(L_) * Bmax * pout);
+  gp_fake_ = DeviceBuf(static_cast<size_t>(L_) * Bmax * pout);
+  for (int par = 0; par < 2; ++par) {
+    for (int k = 0; k < 2; ++k) dz_[par][k] = DeviceBuf(static_cast<size_t>(L_) * Bmax * zcp_);
+    d_idx_[par] = dev_alloc<int>(static_cast<size_t>(L_) * Bmax);
+    h_idx_[par] = pinned<int>(static_cast<size_t>(L_) * Bmax);
+    h_z_[par] = pinned<float>(static_cast<size_t>(2) * L_ * Bmax * zcp_);
+    check_cuda(cudaEventCreateWithFlags(&staged_[par], cudaEventDisableTiming), "event");
+  }
+  check_cuda(cudaEventCreate(&t0_), "event");
+  check_cuda(cudaEventCreate(&t1_), "event");
+  d_flags_ = dev_alloc<int>(static_cast<size_t>(L_));
+  d_t_g_ = dev_alloc<long long>(static_cast<size_t>(L_));
+  d_t_d_ = dev_alloc<long long>(static_cast<size_t>(L_));
+  rep_cap_ = 256;
+  d_rep_ = dev_alloc<double>(static_cast<size_t>(rep_cap_) * L_ * 4);
+  h_rep_ = pinned<double>(static_cast<size_t>(rep_cap_) * L_ * 4);
+  pool_ = std::make_unique<ThreadPool>(std::max(1, cfg_.threads));
+
+  // make_gan_pair per label: G from derive_seed(seed, 1), D from derive_seed(seed, 2) (gan.cpp:39-40)
+  std::vector<float> gp(static_cast<size_t>(L_) * G_->P()), dp(static_cast<size_t>(L_) * D_->P());
+  std::vector<float> gb(static_cast<size_t>(L_) * std::max<long long>(G_->Bf(), 4), 0.f),
+      db(static_cast<size_t>(L_) * std::max<long long>(D_->Bf(), 4), 0.f);
+  pool_->parallel_for(L_, [&](int l) {
+    uint64_t wseed = derive_seed(cfg_.base_seed, static_cast<uint64_t>(cfg_.class_ids[static_cast<size_t>(l)]));
+    auto g = G_->init_ref_params(derive_seed(wseed, 1), cfg_.init_std);
+    auto d = D_->init_ref_params(derive_seed(wseed, 2), cfg_.init_std);
+    G_->import_params(g.data(), gp.data() + static_cast<size_t>(l) * G_->P());
+    D_->import_params(d.data(), dp.data() + static_cast<size_t>(l) * D_->P());
+    auto gbuf = G_->init_ref_buffers(), dbuf = D_->init_ref_buffers();
+    G_->import_buffers(gbuf.data(), gb.data() + static_cast<size_t>(l) * std::max<long long>(G_->Bf(), 4));
+    D_->import_buffers(dbuf.data(), db.data() + static_cast<size_t>(l) * std::max<long long>(D_->Bf(), 4));
+  });
+  check_cuda(cudaMemcpy(G_->params.p, gp.data(), gp.size() * sizeof(float), cudaMemcpyHostToDevice), "upload G");
+  check_cuda(cudaMemcpy(D_->params.p, dp.data(), dp.size() * sizeof(float), cudaMemcpyHostToDevice), "upload D");
+  if (G_->Bf()) check_cuda(cudaMemcpy(G_->running.p, gb.data(), gb.size() * sizeof(float), cudaMemcpyHostToDevice), "upload");
+  if (D_->Bf()) check_cuda(cudaMemcpy(D_->running.p, db.data(), db.size() * sizeof(float), cudaMemcpyHostToDevice), "upload");
+
+  // run_worker: Rng rng(cfg.seed) per label; order = the label's shard
+  rng_.reserve(static_cast<size_t>(L_));
+  for (int l = 0; l < L_; ++l)
+    rng_.emplace_back(derive_seed(cfg_.base_seed, static_cast<uint64_t>(cfg_.class_ids[static_cast<size_t>(l)])));
+  order_.assign(static_cast<size_t>(L_), std::vector<int>(static_cast<size_t>(cfg_.per_label)));
+  for (auto& o : order_)
+    for (long j = 0; j < cfg_.per_label; ++j) o[static_cast<size_t>(j)] = static_cast<int>(j);
+  last_batch_.assign(static_cast<size_t>(L_), {});
+  reports_.assign(static_cast<size_t>(L_), {});
+}
+
+GanGroup::~GanGroup() {
+  if (st_) cudaStreamSynchronize(st_);
+  for (int par = 0; par < 2; ++par) {
+    cudaFree(d_idx_[par]);
+    cudaFreeHost(h_idx_[par]);
+    cudaFreeHost(h_z_[par]);
+    if (staged_[par]) cudaEventDestroy(staged_[par]);
+  }
+  cudaFree(d_flags_);
+  cudaFree(d_t_g_);
+  cudaFree(d_t_d_);
+  cudaFree(d_rep_);
+  cudaFreeHost(h_rep_);
+  if (t0_) cudaEventDestroy(t0_);
+  if (t1_) cudaEventDestroy(t1_);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void GanGroup::set_dataset(const float* images01) {
+  const Map& im = D_->in_map();
+  const long long n = static_cast<long long>(L_) * cfg_.per_label;
+  DeviceBuf tmp(static_cast<size_t>(n) * cfg_.C * cfg_.H * cfg_.W);
+  check_cuda(cudaMemcpyAsync(tmp.p, images01, tmp.n * sizeof(float), cudaMemcpyHostToDevice, st_), "dataset H2D");
+  // resident copy: NHWC padded, raw [0,1] pixels (the per-step gather applies 2x-1)
+  check_cuda(launch_nchw01_to_nhwc(n, static_cast<int>(cfg_.C), static_cast<int>(cfg_.H), static_cast<int>(cfg_.W),
+                                   static_cast<int>(im.Cp), tmp.p, data_.p, st_, 0),
+             "dataset layout");
+  check_cuda(cudaStreamSynchronize(st_), "sync");
+}
+
+void GanGroup::generate_dataset(uint64_t data_seed) {
+  const Map& im = D_->in_map();
+  const long S = cfg_.C * cfg_.H * cfg_.W;
+  std::vector<float> h(static_cast<size_t>(L_) * cfg_.per_label * im.numel(), 0.f);
+  pool_->parallel_for(L_, [&](int l) {
+    std::vector<double> buf(static_cast<size_t>(cfg_.per_label * S));
+    cosine_label(cfg_.C, cfg_.H, cfg_.W, cfg_.per_label, data_seed, cfg_.class_ids[static_cast<size_t>(l)], buf.data());
+    float* o = h.data() + static_cast<size_t>(l) * cfg_.per_label * im.numel();
+    for (long j = 0; j < cfg_.per_label; ++j)
+      for (long c = 0; c < cfg_.C; ++c)
+        for (long y = 0; y < cfg_.H; ++y)
+          for (long x = 0; x < cfg_.W; ++x)
+            o[j * im.numel() + (y * cfg_.W + x) * im.Cp + c] =
+                static_cast<float>(buf[static_cast<size_t>(((j * cfg_.C + c) * cfg_.H + y) * cfg_.W + x)]);
+  });
+  check_cuda(cudaMemcpy(data_.p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice), "dataset upload");
+}
+
+int GanGroup::next_batch_size() const {
+  long start = fresh_epoch_ ? 0 : at_;
+  return static_cast<int>(std::min<long>(cfg_.batch, cfg_.per_label - start));
+}
+
+// Host half of a step for every label (in parallel): the epoch shuffle when
+// one starts (std::shuffle on the label's engine, partition.cpp:91), the next
+// contiguous batch, then z1 and z2 (gan.cpp:150,161).
+void GanGroup::prep_host(int par, int B, bool with_idx) {
+  const bool shuffle = fresh_epoch_;
+  const long start = shuffle ? 0 : at_;
+  int* hidx = h_idx_[par];
+  float* hz = h_z_[par];
+  const long dz = cfg_.d_z;
+  pool_->parallel_for(L_, [&](int l) {
+    Rng& r = rng_[static_cast<size_t>(l)];
+    auto& ord = order_[static_cast<size_t>(l)];
+    if (with_idx) {
+      if (shuffle) std::shuffle(ord.begin(), ord.end(), r.engine());
+      auto& lb = last_batch_[static_cast<size_t>(l)];
+      lb.resize(static_cast<size_t>(B));
+      for (int b = 0; b < B; ++b) {
+        hidx[l * B + b] = ord[static_cast<size_t>(start + b)];
+        lb[static_cast<size_t>(b)] = ord[static_cast<size_t>(start + b)];
+      }
+    }
+    for (int k = 0; k < 2; ++k) {
+      float* z = hz + (static_cast<size_t>(k) * L_ + l) * B * zcp_;
+      for (int b = 0; b < B; ++b)
+        for (long j = 0; j < dz; ++j) z[b * zcp_ + j] = static_cast<float>(r.normal());
+    }
+  });
+  if (with_idx) {
+    at_ = start + B;
+    fresh_epoch_ = false;
+    if (at_ >= cfg_.per_label) {
+      epoch_ += 1;
+      fresh_epoch_ = true;
+      at_ = 0;
+    }
+  }
+}
+
+// The adversarial step (gan.cpp:136-176) for all labels, on st_.
+void GanGroup::enqueue_step(int B, const float* real_nhwc, int par) {
+  const int pstride = static_cast<int>(D_->out_map().Cp);
+  const int nbg = G_->blocks(), nbd = D_->blocks();
+  double* rep = d_rep_ + (steps_ % rep_cap_) * L_ * 4;
+  // discriminator update on (real, fresh fake); the generator trace is dropped
+  tg_.act[0] = dz_[par][0].p;
+  G_->forward(tg_, B, true, true, st_);
+  tdr_.act[0] = const_cast<float*>(real_nhwc);
+  D_->forward(tdr_, B, true, true, st_);
+  tdf_.act[0] = tg_.act[static_cast<size_t>(nbg)];
+  D_->forward(tdf_, B, true, true, st_);
+  check_cuda(launch_loss_d(L_, B, tdr_.act[static_cast<size_t>(nbd)], tdf_.act[static_cast<size_t>(nbd)], pstride,
+                           cfg_.clamp, gp_real_.p, gp_fake_.p, rep, st_),
+             "loss_d");
+  D_->backward(tdr_, B, gp_real_.p, true, false, nullptr, st_);
+  D_->backward(tdf_, B, gp_fake_.p, true, true, nullptr, st_);
+  check_cuda(launch_nonfinite_check(L_, D_->P(), D_->grads.p, d_flags_, st_), "nonfinite D");
+  check_cuda(launch_adam_tick(L_, d_flags_, d_t_d_, st_), "tick D");
+  check_cuda(launch_adam(L_, D_->P(), D_->params.p, D_->grads.p, D_->adam_m.p, D_->adam_v.p, d_t_d_, d_flags_,
+                         static_cast<float>(cfg_.lr), static_cast<float>(cfg_.beta1), static_cast<float>(cfg_.beta2),
+                         static_cast<float>(cfg_.eps), st_),
+             "adam D");
+  // generator update through the updated discriminator (its grads discarded)
+  tg_.act[0] = dz_[par][1].p;
+  G_->forward(tg_, B, true, true, st_);
+  tdf_.act[0] = tg_.act[static_cast<size_t>(nbg)];
+  D_->forward(tdf_, B, true, true, st_);
+  check_cuda(launch_loss_g(L_, B, tdf_.act[static_cast<size_t>(nbd)], pstride, cfg_.clamp, gp_fake_.p, rep, st_),
+             "loss_g");
+  D_->backward(tdf_, B, gp_fake_.p, false, false, gimg_.p, st_);
+  G_->backward(tg_, B, gimg_.p, true, false, nullptr, st_);
+  check_cuda(launch_nonfinite_check(L_, G_->P(), G_->grads.p, d_flags_, st_), "nonfinite G");
+  check_cuda(launch_adam_tick(L_, d_flags_, d_t_g_, st_), "tick G");
+  check_cuda(launch_adam(L_, G_->P(), G_->params.p, G_->grads.p, G_->adam_m.p, G_->adam_v.p, d_t_g_, d_flags_,
+                         static_cast<float>(cfg_.lr), static_cast<float>(cfg_.beta1), static_cast<float>(cfg_.beta2),
+                         static_cast<float>(cfg_.eps), st_),
+             "adam G");
+  steps_ += 1;
+  pending_ += 1;
+  if (pending_ >= rep_cap_) drain_reports();
+}
+
+void GanGroup::drain_reports() {
+  if (pending_ == 0) return;
+  check_cuda(cudaStreamSynchronize(st_), "sync");
+  check_cuda(cudaMemcpy(h_rep_, d_rep_, static_cast<size_t>(rep_cap_) * L_ * 4 * sizeof(double), cudaMemcpyDeviceToHost),
+             "reports D2H");
+  for (long s = steps_ - pending_; s < steps_; ++s) {
+    const double* r = h_rep_ + (s % rep_cap_) * L_ * 4;
+    for (int l = 0; l < L_; ++l)
+      reports_[static_cast<size_t>(l)].push_back(StepReport{r[l * 4], r[l * 4 + 1], r[l * 4 + 2], r[l * 4 + 3]});
+  }
+  pending_ = 0;
+}
+
+int GanGroup::train_steps(int n) {
+  const Map& im = D_->in_map();
+  int done = 0;
+  check_cuda(cudaEventRecord(t0_, st_), "event");
+  for (int s = 0; s < n; ++s) {
+    if (epoch_ >= cfg_.epochs) break;
+    const int par = static_cast<int>(steps_ & 1);
+    const int B = next_batch_size();
+    // the staging slot `par` was last read by the copies of two steps ago
+    check_cuda(cudaEventSynchronize(staged_[par]), "staging wait");
+    prep_host(par, B, true);
+    check_cuda(cudaMemcpyAsync(d_idx_[par], h_idx_[par], sizeof(int) * L_ * B, cudaMemcpyHostToDevice, st_), "idx H2D");
+    const size_t zb = sizeof(float) * static_cast<size_t>(L_) * B * zcp_;
+    check_cuda(cudaMemcpyAsync(dz_[par][0].p, h_z_[par], zb, cudaMemcpyHostToDevice, st_), "z1 H2D");
+    check_cuda(cudaMemcpyAsync(dz_[par][1].p, h_z_[par] + static_cast<size_t>(L_) * B * zcp_, zb,
+                               cudaMemcpyHostToDevice, st_),
+               "z2 H2D");
+    check_cuda(cudaEventRecord(staged_[par], st_), "event");
+    check_cuda(launch_gather_real(L_, B, d_idx_[par], data_.p, static_cast<long long>(cfg_.per_label) * im.numel(),
+                                  im.numel(), static_cast<int>(im.Cp), static_cast<int>(im.C), real_.p, st_),
+               "gather");
+    enqueue_step(B, real_.p, par);
+    ++done;
+  }
+  check_cuda(cudaEventRecord(t1_, st_), "event");
+  check_cuda(cudaEventSynchronize(t1_), "sync");
+  check_cuda(cudaEventElapsedTime(&last_ms_, t0_, t1_), "elapsed");
+  drain_reports();
+  return done;
+}
+
+void GanGroup::train_step_host(const float* real01, int B, double* reports) {
+  if (B < 1 || B > std::min<long>(cfg_.batch, cfg_.per_label)) throw std::invalid_argument("train_step: batch size out of range");
+  const Map& im = D_->in_map();
+  const int par = static_cast<int>(steps_ & 1);
+  check_cuda(cudaEventSynchronize(staged_[par]), "staging wait");
+  prep_host(par, B, false);
+  const size_t zb = sizeof(float) * static_cast<size_t>(L_) * B * zcp_;
+  check_cuda(cudaMemcpyAsync(dz_[par][0].p, h_z_[par], zb, cudaMemcpyHostToDevice, st_), "z1 H2D");
+  check_cuda(cudaMemcpyAsync(dz_[par][1].p, h_z_[par] + static_cast<size_t>(L_) * B * zcp_, zb, cudaMemcpyHostToDevice,
+                             st_),
+             "z2 H2D");
+  // real batch H2D into the gradient scratch (same extent), then NCHW->NHWC with 2x-1
+  const size_t rb = sizeof(float) * static_cast<size_t>(L_) * B * cfg_.C * cfg_.H * cfg_.W;
+  check_cuda(cudaMemcpyAsync(gimg_.p, real01, rb, cudaMemcpyHostToDevice, st_), "real H2D");
+  check_cuda(cudaEventRecord(staged_[par], st_), "event");
+  check_cuda(launch_nchw01_to_nhwc(static_cast<long long>(L_) * B, static_cast<int>(cfg_.C), static_cast<int>(cfg_.H),
+                                   static_cast<int>(cfg_.W), static_cast<int>(im.Cp), gimg_.p, real_.p, st_),
+             "real layout");
+  enqueue_step(B, real_.p, par);
+  drain_reports();
+  if (reports)
+    for (int l = 0; l < L_; ++l) {
+      const StepReport& r = reports_[static_cast<size_t>(l)].back();
+      reports[l * 4 + 0] = r.j_d;
+      reports[l * 4 + 1] = r.j_g;
+      reports[l * 4 + 2] = r.d_real_mean;
+      reports[l * 4 + 3] = r.d_fake_mean;
+    }
+}
+
+void GanGroup::train_step_inputs(const float* real01, const float* z1, const float* z2, int B, double* reports) {
+  if (B < 1 || B > std::min<long>(cfg_.batch, cfg_.per_label)) throw std::invalid_argument("train_step: batch size out of range");
+  const Map& im = D_->in_map();
+  const int par = static_cast<int>(steps_ & 1);
+  check_cuda(cudaEventSynchronize(staged_[par]), "staging wait");
+  float* hz = h_z_[par];
+  for (int k = 0; k < 2; ++k) {
+    const float* src = k == 0 ? z1 : z2;
+    for (long r = 0; r < static_cast<long>(L_) * B; ++r)
+      for (long j = 0; j < zcp_; ++j)
+        hz[(static_cast<size_t>(k) * L_ * B + r) * zcp_ + j] = j < cfg_.d_z ? src[r * cfg_.d_z + j] : 0.f;
+  }
+  const size_t zb = sizeof(float) * static_cast<size_t>(L_) * B * zcp_;
+  check_cuda(cudaMemcpyAsync(dz_[par][0].p, hz, zb, cudaMemcpyHostToDevice, st_), "z1 H2D");
+  check_cuda(cudaMemcpyAsync(dz_[par][1].p, hz + static_cast<size_t>(L_) * B * zcp_, zb, cudaMemcpyHostToDevice, st_),
+             "z2 H2D");
+  const size_t rb = sizeof(float) * static_cast<size_t>(L_) * B * cfg_.C * cfg_.H * cfg_.W;
+  check_cuda(cudaMemcpyAsync(gimg_.p, real01, rb, cudaMemcpyHostToDevice, st_), "real H2D");
+  check_cuda(cudaEventRecord(staged_[par], st_), "event");
+  check_cuda(launch_nchw01_to_nhwc(static_cast<long long>(L_) * B, static_cast<int>(cfg_.C), static_cast<int>(cfg_.H),
+                                   static_cast<int>(cfg_.W), static_cast<int>(im.Cp), gimg_.p, real_.p, st_),
+             "real layout");
+  enqueue_step(B, real_.p, par);
+  drain_reports();
+  if (reports)
+    for (int l = 0; l < L_; ++l) {
+      const StepReport& r = reports_[static_cast<size_t>(l)].back();
+      reports[l * 4 + 0] = r.j_d;
+      reports[l * 4 + 1] = r.j_g;
+      reports[l * 4 + 2] = r.d_real_mean;
+      reports[l * 4 + 3] = r.d_fake_mean;
+    }
+}
+
+void GanGroup::sync() {
+  check_cuda(cudaStreamSynchronize(st_), "sync");
+  drain_reports();
+}
+
+std::vector<int> GanGroup::failed() {
+  sync();
+  std::vector<int> f(static_cast<size_t>(L_));
+  check_cuda(cudaMemcpy(f.data(), d_flags_, sizeof(int) * L_, cudaMemcpyDeviceToHost), "flags");
+  return f;
+}
+
+long GanGroup::get(int label, int what, double* out, long cap) {
+  if (label < 0 || label >= L_) throw std::out_of_range("label index " + std::to_string(label));
+  sync();
+  auto fetch = [&](DevNet& net, const DeviceBuf& arena, bool buffers) -> long {
+    long n = buffers ? net.ref_buffers() : net.ref_params();
+    if (!out) return n;
+    if (cap < n) throw std::invalid_argument("output buffer too small");
+    long long per = buffers ? std::max<long long>(net.Bf(), 4) : net.P();
+    std::vector<float> h(static_cast<size_t>(per));
+    check_cuda(cudaMemcpy(h.data(), arena.p + static_cast<size_t>(label) * per, per * sizeof(float), cudaMemcpyDeviceToHost),
+               "readback");
+    if (buffers) net.export_buffers(h.data(), out);
+    else net.export_params(h.data(), out);
+    return n;
+  };
+  switch (what) {
+    case G_PARAMS: return fetch(*G_, G_->params, false);
+    case D_PARAMS: return fetch(*D_, D_->params, false);
+    case G_BUFFERS: return fetch(*G_, G_->running, true);
+    case D_BUFFERS: return fetch(*D_, D_->running, true);
+    case G_GRADS: return fetch(*G_, G_->grads, false);
+    case D_GRADS: return fetch(*D_, D_->grads, false);
+    case G_M: return fetch(*G_, G_->adam_m, false);
+    case G_V: return fetch(*G_, G_->adam_v, false);
+    case D_M: return fetch(*D_, D_->adam_m, false);
+    case D_V: return fetch(*D_, D_->adam_v, false);
+    case REPORTS: {
+      const auto& r = reports_[static_cast<size_t>(label)];
+      long n = static_cast<long>(r.size()) * 4;
+      if (out) {
+        if (cap < n) throw std::invalid_argument("output buffer too small");
+        for (size_t i = 0; i < r.size(); ++i) {
+          out[i * 4] = r[i].j_d;
+          out[i * 4 + 1] = r[i].j_g;
+          out[i * 4 + 2] = r[i].d_real_mean;
+          out[i * 4 + 3] = r[i].d_fake_mean;
+        }
+      }
+      return n;
+    }
+    case LAST_BATCH: {
+      const auto& b = last_batch_[static_cast<size_t>(label)];
+      if (out) {
+        if (cap < static_cast<long>(b.size())) throw std::invalid_argument("output buffer too small");
+        for (size_t i = 0; i < b.size(); ++i) out[i] = static_cast<double>(b[i]);
+      }
+      return static_cast<long>(b.size());
+    }
+    case COUNTERS: {
+      long long tg = 0, td = 0;
+      check_cuda(cudaMemcpy(&tg, d_t_g_ + label, sizeof(tg), cudaMemcpyDeviceToHost), "t");
+      check_cuda(cudaMemcpy(&td, d_t_d_ + label, sizeof(td), cudaMemcpyDeviceToHost), "t");
+      if (out) {
+        if (cap < 3) throw std::invalid_argument("output buffer too small");
+        out[0] = static_cast<double>(tg);
+        out[1] = static_cast<double>(td);
+        out[2] = static_cast<double>(steps_);
+      }
+      return 3;
+    }
+  }
+  throw std::invalid_argument("unknown field code " + std::to_string(what));
+}
+
+void GanGroup::set(int label, int what, const double* in, long n) {
+  if (label < 0 || label >= L_) throw std::out_of_range("label index " + std::to_string(label));
+  sync();
+  auto put = [&](DevNet& net, DeviceBuf& arena, bool buffers) {
+    long want = buffers ? net.ref_buffers() : net.ref_params();
+    if (n != want) throw std::invalid_argument("length mismatch on set");
+    long long per = buffers ? std::max<long long>(net.Bf(), 4) : net.P();
+    std::vector<float> h(static_cast<size_t>(per));
+    if (buffers) net.import_buffers(in, h.data());
+    else net.import_params(in, h.data());
+    check_cuda(cudaMemcpy(arena.p + static_cast<size_t>(label) * per, h.data(), per * sizeof(float), cudaMemcpyHostToDevice),
+               "upload");
+  };
+  switch (what) {
+    case G_PARAMS: put(*G_, G_->params, false); return;
+    case D_PARAMS: put(*D_, D_->params, false); return;
+    case G_BUFFERS: put(*G_, G_->running, true); return;
+    case D_BUFFERS: put(*D_, D_->running, true); return;
+  }
+  throw std::invalid_argument("field not settable: " + std::to_string(what));
+}
+
+void GanGroup::generate(long n, uint64_t seed, float* out) {
+  sync();
+  const int Bmax = static_cast<int>(std::min<long>(cfg_.batch, cfg_.per_label));
+  const Map& om = G_->out_map();
+  std::vector<Rng> rs;
+  for (int l = 0; l < L_; ++l) rs.emplace_back(derive_seed(seed, static_cast<uint64_t>(cfg_.class_ids[static_cast<size_t>(l)])));
+  DeviceBuf o(static_cast<size_t>(L_) * Bmax * cfg_.C * cfg_.H * cfg_.W);
+  std::vector<float> zh(static_cast<size_t>(L_) * Bmax * zcp_, 0.f), oh(o.n);
+  for (long done = 0; done < n; done += Bmax) {
+    int B = static_cast<int>(std::min<long>(Bmax, n - done));
+    pool_->parallel_for(L_, [&](int l) {
+      for (int b = 0; b < B; ++b)
+        for (long j = 0; j < cfg_.d_z; ++j)
+          zh[(static_cast<size_t>(l) * B + b) * zcp_ + j] = static_cast<float>(rs[static_cast<size_t>(l)].normal());
+    });
+    check_cuda(cudaMemcpyAsync(dz_[0][0].p, zh.data(), sizeof(float) * L_ * B * zcp_, cudaMemcpyHostToDevice, st_), "z");
+    tg_.act[0] = dz_[0][0].p;
+    G_->forward(tg_, B, false, false, st_);
+    check_cuda(launch_nhwc_to_nchw01(static_cast<long long>(L_) * B, static_cast<int>(cfg_.C), static_cast<int>(cfg_.H),
+                                     static_cast<int>(cfg_.W), static_cast<int>(om.Cp),
+                                     tg_.act[static_cast<size_t>(G_->blocks())], o.p, st_),
+               "to nchw");
+    check_cuda(cudaMemcpyAsync(oh.data(), o.p, sizeof(float) * L_ * B * cfg_.C * cfg_.H * cfg_.W,
+                               cudaMemcpyDeviceToHost, st_),
+               "samples D2H");
+    check_cuda(cudaStreamSynchronize(st_), "sync");
+    const long S = cfg_.C * cfg_.H * cfg_.W;
+    for (int l = 0; l < L_; ++l)
+      std::memcpy(out + (static_cast<size_t>(l) * n + done) * S, oh.data() + static_cast<size_t>(l) * B * S,
+                  sizeof(float) * B * S);
+  }
+}
+
+}  // namespace pg

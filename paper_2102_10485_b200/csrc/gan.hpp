@@ -1,0 +1,121 @@
+// Label group trainer: the B200 form of partgan's worker loop and adversarial
+// step for all L labels resident on one GPU.
+//
+//   reference                                   here
+//   run_worker (partition.cpp:78-112)           GanGroup: one Rng + shuffle order per label, host side
+//   train_step / step_impl (gan.cpp:136-182)    GanGroup::enqueue_step: the same D-then-G sequence, every
+//                                               kernel batched over the L labels in lockstep
+//   adam_step (optim.cpp:20-34)                 non-finite check + Adam over the [L][P] arenas
+//   TrainError (partition.hpp:63-69)            per-label failure flags (a label whose gradients went
+//                                               non-finite stops updating, exactly like a failed worker)
+//
+// Labels never exchange data; grouping changes the launch shape, not the math.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host_util.hpp"
+#include "net.hpp"
+#include "rng.hpp"
+
+namespace pg {
+
+struct GroupConfig {
+  std::string gen_spec, disc_spec;
+  long C = 1, H = 28, W = 28;
+  long d_z = 100;
+  std::vector<int> class_ids;  // labels of this group
+  uint64_t base_seed = 1;      // worker seed = derive_seed(base_seed, class_id)  (run.cpp:376)
+  int batch = 64;
+  int epochs = 1;
+  long per_label = 64;         // shard size of every label
+  double lr = 2e-4, beta1 = 0.5, beta2 = 0.999, eps = 1e-8;
+  double clamp = 1e-7, init_std = 0.02;
+  int math = MATH_FP32_SIMT;
+  int threads = 8;
+};
+
+struct StepReport {
+  double j_d = 0, j_g = 0, d_real_mean = 0, d_fake_mean = 0;
+};
+
+class GanGroup {
+ public:
+  explicit GanGroup(const GroupConfig& cfg);
+  ~GanGroup();
+
+  int L() const { return L_; }
+  const GroupConfig& config() const { return cfg_; }
+  DevNet& gen() { return *G_; }
+  DevNet& disc() { return *D_; }
+  cudaStream_t stream() const { return st_; }
+
+  // dataset: [L][per_label][C][H][W] in [0,1] (host, f32) -> device NHWC
+  void set_dataset(const float* images01);
+  void generate_dataset(uint64_t data_seed);
+
+  // the worker protocol on the device-resident dataset: per label shuffle at
+  // each epoch start, contiguous batches (partial tail kept), z1 then z2.
+  // Returns the number of steps actually run (stops when every epoch is done).
+  int train_steps(int n);
+  // steps on host-provided real batches (the reference train_step call):
+  // real01 [L][B][C][H][W] in [0,1]; latents from each label's stream.
+  void train_step_host(const float* real01, int B, double* reports);
+  // fully explicit inputs (no stream use): z1, z2 [L][B][d_z]
+  void train_step_inputs(const float* real01, const float* z1, const float* z2, int B, double* reports);
+
+  // reference-layout readback of one label (f64)
+  enum Field { G_PARAMS = 0, D_PARAMS, G_BUFFERS, D_BUFFERS, G_GRADS, D_GRADS, G_M, G_V, D_M, D_V, REPORTS, LAST_BATCH, COUNTERS };
+  long get(int label, int what, double* out, long cap);
+  void set(int label, int what, const double* in, long n);
+  std::vector<int> failed();
+  // eval-mode samples: n per label with latents from Rng(derive_seed(seed, class_id)),
+  // (v+1)/2 mapped, out [L][n][C][H][W]
+  void generate(long n, uint64_t seed, float* out);
+  void sync();
+  long steps_done() const { return steps_; }
+
+  // time of the last train_steps() call on the device (ms, CUDA events)
+  float last_device_ms() const { return last_ms_; }
+
+ private:
+  GroupConfig cfg_;
+  int L_;
+  std::unique_ptr<DevNet> G_, D_;
+  Trace tg_, tdr_, tdf_;
+  cudaStream_t st_ = nullptr;
+  DeviceBuf data_, dz_[2][2], real_, gp_real_, gp_fake_, gimg_;
+  int* d_idx_[2] = {nullptr, nullptr};
+  int* d_flags_ = nullptr;
+  long long* d_t_g_ = nullptr;
+  long long* d_t_d_ = nullptr;
+  double* d_rep_ = nullptr;
+  // pinned staging
+  int* h_idx_[2] = {nullptr, nullptr};
+  float* h_z_[2] = {nullptr, nullptr};
+  double* h_rep_ = nullptr;
+  long rep_cap_ = 0;
+  cudaEvent_t staged_[2] = {nullptr, nullptr};
+  cudaEvent_t t0_ = nullptr, t1_ = nullptr;
+  std::unique_ptr<ThreadPool> pool_;
+  // per-label host state (run_worker)
+  std::vector<Rng> rng_;
+  std::vector<std::vector<int>> order_;
+  std::vector<std::vector<long>> last_batch_;
+  int epoch_ = 0;
+  long at_ = 0;
+  bool fresh_epoch_ = true;
+  long steps_ = 0, pending_ = 0;
+  std::vector<std::vector<StepReport>> reports_;
+  float last_ms_ = 0.f;
+  long zcp_ = 0;  // padded latent width
+
+  int next_batch_size() const;
+  void prep_host(int par, int B, bool with_idx);
+  void enqueue_step(int B, const float* real_nhwc, int par);
+  void drain_reports();
+};
+
+}  // namespace pg

@@ -1,0 +1,98 @@
+// Internal launchers (C++ linkage).  The C-ABI in include/pg_kernels.h wraps
+// these; the device network (net.cpp) calls them directly.
+#pragma once
+
+#include "common.cuh"
+
+namespace pg {
+
+enum MathMode : int { MATH_FP32_SIMT = 0, MATH_TF32X3 = 1, MATH_TF32 = 2 };
+
+// every launcher ends with `return launched();`: counts the kernel launch
+// (bench.py's gpu_launches) and returns the launch status
+cudaError_t launched();
+long long launch_count();
+// optional per-GEMM timing (CUDA events on the launching stream)
+void gemm_timing_enable(bool on);
+double gemm_timing_read_ms();
+
+int gemm_max_m(const GemmArgs& a);
+int gemm_n(const GemmArgs& a);
+cudaError_t launch_gemm_simt(const GemmArgs& a, cudaStream_t st);
+cudaError_t launch_gemm_tc(const GemmArgs& a, int math, cudaStream_t st);  // tcgen05 engine
+bool gemm_tc_supported(const GemmArgs& a);
+// picks the engine for a math mode and problem shape
+cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st);
+
+// ---- per-channel reductions over [L][R][Cp] maps (deterministic two-level) ----
+enum ReduceMode : int {
+  RED_SUM = 0,      // s0 = sum x
+  RED_SQDEV = 1,    // s0 = sum (x - mean)^2
+  RED_BN_BWD = 2,   // g1 = act_bwd(gy, y); s0 = sum g1; s1 = sum g1 (x-mean); s2 = sum (x-mean)
+  RED_ACT_G = 3,    // g1 = act_bwd(gy, y); s0 = sum g1
+};
+struct ChannelMap {
+  int L, R, Cp, C;         // rows per label, padded / valid channels
+  long long ls;            // label stride of the maps (floats)
+};
+int reduce_chunks(int R);
+size_t reduce_partial_floats(const ChannelMap& cm);
+// partial: [L][chunks][3][Cp]
+cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x, const float* gy, const float* y,
+                                  const float* mean, int act, float slope, float* partial, cudaStream_t st);
+
+// BN forward finalize: pass 0 -> mean; pass 1 -> var, inv_std, running-stat update.
+cudaError_t launch_bn_finalize_mean(const ChannelMap& cm, const float* partial, float* mean, cudaStream_t st);
+cudaError_t launch_bn_finalize_var(const ChannelMap& cm, const float* partial, const float* mean, float* istd,
+                                   float* running, long long run_ls, float eps, float momentum, int update_running,
+                                   cudaStream_t st);
+// y = act(gamma (x - mean) istd + beta); eval mode passes running stats as mean/istd source.
+cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* mean, const float* istd,
+                            const float* gamma_beta, long long gb_ls, int act, float slope, float* y, cudaStream_t st);
+// eval-mode: istd from running var
+cudaError_t launch_bn_eval_stats(const ChannelMap& cm, const float* running, long long run_ls, float eps, float* mean,
+                                 float* istd, cudaStream_t st);
+// BN backward: from RED_BN_BWD partials build per-channel coefficients and
+// write dgamma/dbeta (+ the preceding layer's bias grad) into the grad arena.
+cudaError_t launch_bn_bwd_finalize(const ChannelMap& cm, const float* partial, const float* istd,
+                                   const float* gamma_beta, long long gb_ls, float* dgamma_beta, long long dgb_ls,
+                                   float* dbias, long long dbias_ls, int accumulate, int train, float* coef,
+                                   cudaStream_t st);
+// gz = act_bwd(gy, y) * gamma istd + dvar 2 (x - mean)/m + dmean/m
+cudaError_t launch_bn_bwd_apply(const ChannelMap& cm, const float* gy, const float* y, const float* x,
+                                const float* mean, const float* coef, int act, float slope, float* gz,
+                                cudaStream_t st);
+// g = act_bwd(gy, y) elementwise (in place allowed)
+cudaError_t launch_act_bwd(const ChannelMap& cm, const float* gy, const float* y, int act, float slope, float* g,
+                           cudaStream_t st);
+// bias grad from RED_SUM / RED_ACT_G partials
+cudaError_t launch_bias_finalize(const ChannelMap& cm, const float* partial, float* dbias, long long dbias_ls,
+                                 int accumulate, cudaStream_t st);
+
+// ---- GAN losses (gan.cpp:86-132) ----
+// p maps are [L][B][pstride] with the probability in channel 0.
+cudaError_t launch_loss_d(int L, int B, const float* p_real, const float* p_fake, int pstride, double clamp,
+                          float* g_real, float* g_fake, double* report, cudaStream_t st);
+cudaError_t launch_loss_g(int L, int B, const float* p_fake, int pstride, double clamp, float* g, double* report,
+                          cudaStream_t st);
+
+// ---- Adam over [L][P] arenas (optim.cpp:20-34) ----
+cudaError_t launch_nonfinite_check(int L, long long P, const float* grads, int* flags, cudaStream_t st);
+cudaError_t launch_adam_tick(int L, const int* flags, long long* t, cudaStream_t st);
+cudaError_t launch_adam(int L, long long P, float* params, const float* grads, float* m, float* v,
+                        const long long* t, const int* flags, float lr, float b1, float b2, float eps,
+                        cudaStream_t st);
+
+// ---- data movement ----
+// out[l][b][hw][c] = 2 * data[l][idx[l][b]][hw][c] - 1 (c < C), 0 in pad channels
+cudaError_t launch_gather_real(int L, int B, const int* idx, const float* data, long long data_ls, long long sample,
+                               int Cp, int C, float* out, cudaStream_t st);
+// NCHW [N][C][H][W] (values in [0,1]) -> NHWC padded; map2x1 applies 2x-1
+cudaError_t launch_nchw01_to_nhwc(long long N, int C, int H, int W, int Cp, const float* in, float* out,
+                                  cudaStream_t st, int map2x1 = 1);
+// NHWC padded (tanh range) -> NCHW, mapped (v+1)/2
+cudaError_t launch_nhwc_to_nchw01(long long N, int C, int H, int W, int Cp, const float* in, float* out,
+                                  cudaStream_t st);
+cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t st);
+
+}  // namespace pg

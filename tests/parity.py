@@ -1,0 +1,87 @@
+"""Shared helpers for the GPU parity tests: reference <-> device layout
+conversion and the tolerance metrics (documented in DESIGN.md §parity)."""
+from __future__ import annotations
+
+import numpy as np
+
+
+def pad4(c: int) -> int:
+    return (c + 3) // 4 * 4
+
+
+def rel_max(a: np.ndarray, ref: np.ndarray) -> float:
+    """max |a - ref| / max |ref| — per-tensor relative error (grads, outputs)."""
+    a = np.asarray(a, np.float64).ravel()
+    ref = np.asarray(ref, np.float64).ravel()
+    scale = max(np.abs(ref).max(initial=0.0), 1e-30)
+    return float(np.abs(a - ref).max(initial=0.0) / scale)
+
+
+def rel_l2(a: np.ndarray, ref: np.ndarray) -> float:
+    """||a - ref|| / ||ref|| — per-tensor relative error for updated weights
+    (Adam's first steps are ~lr * sign(g), so a rare sign disagreement on a
+    near-zero gradient moves one element by 2*lr; the L2 form weighs that
+    by its share of the tensor)."""
+    a = np.asarray(a, np.float64).ravel()
+    ref = np.asarray(ref, np.float64).ravel()
+    return float(np.linalg.norm(a - ref) / max(np.linalg.norm(ref), 1e-30))
+
+
+def nchw_to_nhwc(x: np.ndarray, cp: int | None = None) -> np.ndarray:
+    """[N][C][H][W] -> [N][H][W][Cp] with zero pad channels."""
+    n, c, h, w = x.shape
+    cp = cp or pad4(c)
+    out = np.zeros((n, h, w, cp), x.dtype)
+    out[..., :c] = x.transpose(0, 2, 3, 1)
+    return out
+
+
+def nhwc_to_nchw(x: np.ndarray, c: int) -> np.ndarray:
+    return np.ascontiguousarray(x[..., :c].transpose(0, 3, 1, 2))
+
+
+def conv_w_to_dev(w: np.ndarray, cout: int, cin: int, k: int) -> np.ndarray:
+    """reference Conv2d weight [Cout][Cin][k][k] -> device [pad4(Cout)][k][k][pad4(Cin)]"""
+    d = np.zeros((pad4(cout), k, k, pad4(cin)), w.dtype)
+    d[:cout, :, :, :cin] = w.reshape(cout, cin, k, k).transpose(0, 2, 3, 1)
+    return d
+
+
+def conv_w_from_dev(d: np.ndarray, cout: int, cin: int, k: int) -> np.ndarray:
+    return np.ascontiguousarray(d.reshape(pad4(cout), k, k, pad4(cin))[:cout, :, :, :cin].transpose(0, 3, 1, 2))
+
+
+def convT_w_to_dev(w: np.ndarray, cin: int, cout: int, k: int) -> np.ndarray:
+    """reference ConvTranspose2d weight [Cin][Cout][k][k] -> device [pad4(Cin)][k][k][pad4(Cout)]"""
+    d = np.zeros((pad4(cin), k, k, pad4(cout)), w.dtype)
+    d[:cin, :, :, :cout] = w.reshape(cin, cout, k, k).transpose(0, 2, 3, 1)
+    return d
+
+
+def convT_w_from_dev(d: np.ndarray, cin: int, cout: int, k: int) -> np.ndarray:
+    return np.ascontiguousarray(d.reshape(pad4(cin), k, k, pad4(cout))[:cin, :, :, :cout].transpose(0, 3, 1, 2))
+
+
+def layer_tensors(spec: str, in_shape: tuple) -> list[tuple[str, int, int, bool]]:
+    """(name, offset, size, feeds_bn) of every parameter tensor of a layer
+    list in the reference flat layout; feeds_bn marks a linear-layer bias
+    followed by BatchNorm (its exact gradient is zero)."""
+    items = [t.split() for t in spec.split(";") if t.split()]
+    out, off = [], 0
+    for i, tok in enumerate(items):
+        nxt = [t[0] for t in items[i + 1:i + 3]]
+        feeds_bn = "bn" in nxt[:1] or (nxt[:1] == ["reshape"] and "bn" in nxt[1:2])
+        if tok[0] == "dense":
+            a, b = int(tok[1]), int(tok[2])
+            out += [(f"{i}.dense.w", off, a * b, False), (f"{i}.dense.b", off + a * b, b, feeds_bn)]
+            off += a * b + b
+        elif tok[0] in ("conv2d", "convT2d"):
+            a, b, k = int(tok[1]), int(tok[2]), int(tok[3])
+            n = a * b * k * k
+            out += [(f"{i}.{tok[0]}.w", off, n, False), (f"{i}.{tok[0]}.b", off + n, b, feeds_bn)]
+            off += n + b
+        elif tok[0] == "bn":
+            c = int(tok[1])
+            out += [(f"{i}.bn.gamma", off, c, False), (f"{i}.bn.beta", off + c, c, False)]
+            off += 2 * c
+    return out

@@ -1,0 +1,140 @@
+"""Full training-step parity: the device label group vs the CPU oracle's
+run_worker protocol on identical seeds (same cosine-field data, same
+per-label streams, same init).  North-star bars:
+  - minibatch indices bit-exact;
+  - single-step losses / parameter gradients / updated weights within 1e-4
+    relative (fp32-accurate modes);
+  - 10-step loss trajectories within 1e-3.
+Metrics (tests/parity.py): losses and gradients per tensor max|a-b|/max|ref|;
+updated weights and BN running buffers per tensor ||a-b||/||ref||.  Biases of
+layers that feed a train-mode BatchNorm have an exact gradient of zero (BN
+removes the per-channel mean), so both sides hold rounding noise there; they
+are checked as |g| <= 1e-5 max|g_W| instead and their updates as |dp| <= 2 lr.
+"""
+import numpy as np
+import pytest
+
+from paper_2102_10485_b200 import GroupSpec, LabelGroup, _native as N, baseline_arch
+from parity import layer_tensors, rel_l2, rel_max
+
+pytestmark = pytest.mark.gpu
+
+# oracle field codes match pg_group_get codes 0..12
+OR = dict(gp=0, dp=1, gb=2, db=3, gg=4, dg=5, reports=10, batch=11)
+
+
+def make_pair(cfg, n_labels, per_label, batch, math, epochs=1, first_label=0, threads=8):
+    arch = baseline_arch(cfg)
+    grp = LabelGroup(GroupSpec(arch=arch, class_ids=list(range(first_label, first_label + n_labels)), batch=batch,
+                               epochs=epochs, per_label=per_label, base_seed=7, math=math, threads=threads))
+    grp.generate_dataset(3)
+    return arch, grp
+
+
+def compare_pair_state(grp, orc, arch, n_labels, tol_grad=1e-4, tol_w=1e-4, lr=2e-4):
+    worst = {}
+    for l in range(n_labels):
+        for net, pcode, gcode, bcode, spec, ishape in (
+                ("G", N.F_GEN_PARAMS, N.F_GEN_GRADS, N.F_GEN_BUFFERS, arch.gen, (arch.d_z,)),
+                ("D", N.F_DISC_PARAMS, N.F_DISC_GRADS, N.F_DISC_BUFFERS, arch.disc, arch.image)):
+            gp, rp = grp.get(l, pcode), orc.get(l, pcode)
+            gg, rg = grp.get(l, gcode), orc.get(l, gcode)
+            assert gp.shape == rp.shape and gg.shape == rg.shape
+            tensors = layer_tensors(spec, ishape)
+            wscale = {}
+            for name, off, n, feeds_bn in tensors:
+                if name.endswith(".w"):
+                    wscale[name.split(".")[0]] = np.abs(rg[off:off + n]).max()
+            for name, off, n, feeds_bn in tensors:
+                sl = slice(off, off + n)
+                if feeds_bn:
+                    scale = wscale[name.split(".")[0]]
+                    assert np.abs(gg[sl]).max() <= 1e-5 * scale + 1e-12, (net, name)
+                    assert np.abs(rg[sl]).max() <= 1e-5 * scale + 1e-12, (net, name)
+                    assert np.abs(gp[sl] - rp[sl]).max() <= 2 * lr * max(1, grp_steps(grp, l)), (net, name)
+                    continue
+                eg, ew = rel_max(gg[sl], rg[sl]), rel_l2(gp[sl], rp[sl])
+                worst[f"{net}.{name}.grad"] = max(worst.get(f"{net}.{name}.grad", 0), eg)
+                worst[f"{net}.{name}.param"] = max(worst.get(f"{net}.{name}.param", 0), ew)
+            if net == "G" or True:
+                gb, rb = grp.get(l, bcode), orc.get(l, bcode)
+                if rb.size:
+                    worst[f"{net}.buffers"] = max(worst.get(f"{net}.buffers", 0), rel_l2(gb, rb))
+    bad = {k: v for k, v in worst.items() if v > (tol_grad if k.endswith(".grad") else tol_w)}
+    assert not bad, bad
+    return worst
+
+
+def grp_steps(grp, l):
+    return int(grp.get(l, N.F_COUNTERS)[2])
+
+
+@pytest.mark.parametrize("math", [0, 1])
+@pytest.mark.parametrize("cfg,n_labels,per_label,batch", [(1, 2, 128, 64), (2, 2, 64, 16), (4, 2, 8, 4)])
+def test_single_step_parity(oracle, cfg, n_labels, per_label, batch, math):
+    arch, grp = make_pair(cfg, n_labels, per_label, batch, math)
+    orc = oracle.OracleGroup(64, cfg, n_labels, per_label, batch, data_seed=3, base_seed=7)
+    # initial state identical to build_network's draws (cast to fp32)
+    for l in range(n_labels):
+        assert rel_max(grp.get(l, N.F_GEN_PARAMS), orc.get(l, OR["gp"])) < 1e-7
+        assert rel_max(grp.get(l, N.F_DISC_PARAMS), orc.get(l, OR["dp"])) < 1e-7
+    assert grp.train_steps(1) == 1
+    orc.step(1)
+    for l in range(n_labels):
+        # minibatch indices: bit-exact
+        assert np.array_equal(grp.get(l, N.F_LAST_BATCH), orc.get(l, OR["batch"]))
+        r, q = grp.reports(l)[-1], orc.get(l, OR["reports"]).reshape(-1, 4)[-1]
+        assert abs(r[0] - q[0]) <= 1e-4 * abs(q[0]), (r, q)   # J_D
+        assert abs(r[1] - q[1]) <= 1e-4 * abs(q[1]), (r, q)   # J_G
+        assert abs(r[2] - q[2]) <= 1e-4 * abs(q[2])
+        assert abs(r[3] - q[3]) <= 1e-4 * abs(q[3])
+    compare_pair_state(grp, orc, arch, n_labels)
+    assert not grp.failed().any()
+
+
+def test_ten_step_trajectory_and_ragged_tail(oracle):
+    """10 steps of c1 over two epochs with a partial tail batch each epoch
+    (per_label 80, batch 16 -> 5 full steps per epoch; per_label 72 ->
+    4 full + 1 of 8): indices bit-exact at every step, losses within 1e-3."""
+    for per_label in (80, 72):
+        arch, grp = make_pair(1, 2, per_label, 16, 0, epochs=2)
+        orc = oracle.OracleGroup(64, 1, 2, per_label, 16, data_seed=3, base_seed=7, epochs=2)
+        for s in range(10):
+            assert grp.train_steps(1) == 1
+            orc.step(1)
+            for l in range(2):
+                assert np.array_equal(grp.get(l, N.F_LAST_BATCH), orc.get(l, OR["batch"])), (per_label, s)
+        for l in range(2):
+            r = grp.reports(l)
+            q = orc.get(l, OR["reports"]).reshape(-1, 4)
+            assert r.shape == q.shape == (10, 4)
+            err = np.abs(r - q) / np.maximum(np.abs(q), 1e-12)
+            assert err[:, :2].max() < 1e-3, err
+        # the epoch budget is honoured: no more steps after 2 epochs
+        assert grp.train_steps(5) == 0
+
+
+def test_host_batch_step_matches_explicit_inputs(oracle):
+    """The reference train_step call shape: real batch from host memory with
+    explicit latents, vs the oracle's step on the same inputs."""
+    arch, grp = make_pair(1, 2, 64, 32, 0)
+    orc = oracle.OracleGroup(64, 1, 2, 64, 32, data_seed=3, base_seed=7)
+    rng = np.random.default_rng(0)
+    real = rng.uniform(0, 1, (2, 32) + arch.image)
+    z1, z2 = rng.normal(size=(2, 32, 100)), rng.normal(size=(2, 32, 100))
+    rep = grp.train_step_inputs(real, z1, z2)
+    for l in range(2):
+        q = orc.step_inputs(l, real[l], z1[l], z2[l])
+        assert np.all(np.abs(rep[l] - q) <= 1e-4 * np.abs(q)), (rep[l], q)
+    compare_pair_state(grp, orc, arch, 2)
+
+
+def test_generate_eval_mode(oracle):
+    """generate(): eval-mode BN, (v+1)/2 range, deterministic per seed."""
+    arch, grp = make_pair(1, 2, 64, 32, 0)
+    grp.train_steps(1)
+    a, b = grp.generate(40, seed=5), grp.generate(40, seed=5)
+    assert a.shape == (2, 40, 1, 28, 28)
+    assert np.array_equal(a, b)
+    assert a.min() >= 0 and a.max() <= 1
+    assert a.std() > 0
