@@ -115,7 +115,7 @@ int pg_gen_loss(int L, int B, const float* p_fake, int pstride, double clamp, fl
  * pg_adam_step first scans the gradients for non-finite values (setting flags),
  * then advances t[l] and updates every non-flagged label. */
 int pg_adam_step(int L, long long P, float* params, const float* grads, float* m, float* v, long long* t, int* flags,
-                 float lr, float beta1, float beta2, float eps, void* stream);
+                 double lr, double beta1, double beta2, double eps, void* stream);
 
 /* ---- Real-batch gather (Dataset::gather + 2x-1, data.cpp:13-23, gan.cpp:141) ----
  * data [L][n][sample] (sample = H*W*Cp floats in [0,1]), idx [L][B] row indices,

@@ -68,7 +68,8 @@ _SIGNATURES = {
     "pg_act_bwd": (C.c_int, [_LL, _P, _P, C.c_int, C.c_float, _P, _P]),
     "pg_gan_losses": (C.c_int, [C.c_int, C.c_int, _P, _P, C.c_int, C.c_double, _P, _P, _P, _P]),
     "pg_gen_loss": (C.c_int, [C.c_int, C.c_int, _P, C.c_int, C.c_double, _P, _P, _P]),
-    "pg_adam_step": (C.c_int, [C.c_int, _LL, _P, _P, _P, _P, _P, _P, C.c_float, C.c_float, C.c_float, C.c_float, _P]),
+    "pg_adam_step": (C.c_int, [C.c_int, _LL, _P, _P, _P, _P, _P, _P, C.c_double, C.c_double, C.c_double, C.c_double,
+                               _P]),
     "pg_gather_real": (C.c_int, [C.c_int, C.c_int, _P, _P, _LL, _LL, C.c_int, C.c_int, _P, _P]),
     "pg_group_create": (C.c_int, [C.POINTER(GroupConfig), C.POINTER(_P)]),
     "pg_group_destroy": (None, [_P]),

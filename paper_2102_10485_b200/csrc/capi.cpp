@@ -363,12 +363,14 @@ int pg_gen_loss(int L, int B, const float* p_fake, int pstride, double clamp, fl
 }
 
 int pg_adam_step(int L, long long P, float* params, const float* grads, float* m, float* v, long long* t, int* flags,
-                 float lr, float beta1, float beta2, float eps, void* stream) {
+                 double lr, double beta1, double beta2, double eps, void* stream) {
   return guard([&] {
     if (P % 4) throw std::invalid_argument("adam_step: arena length must be a multiple of 4");
     cuda_ok(pg::launch_nonfinite_check(L, P, grads, flags, S(stream)), "adam");
     cuda_ok(pg::launch_adam_tick(L, flags, t, S(stream)), "adam");
-    cuda_ok(pg::launch_adam(L, P, params, grads, m, v, t, flags, lr, beta1, beta2, eps, S(stream)), "adam");
+    cuda_ok(pg::launch_adam(L, P, params, grads, m, v, t, flags, static_cast<float>(lr), beta1, beta2,
+                            static_cast<float>(eps), S(stream)),
+            "adam");
   });
 }
 

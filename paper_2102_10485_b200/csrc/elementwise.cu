@@ -162,13 +162,15 @@ __global__ void bn_bwd_finalize_kernel(ChannelMap cm, const float* partial, cons
   cf[0] = a;
   cf[1] = 2.f * dvar / m;
   cf[2] = dmean / m;
-  float* dgp = dgb + (long long)l * dgb_ls;
-  if (accumulate) {
-    dgp[c] += dg;
-    dgp[cm.C + c] += db;
-  } else {
-    dgp[c] = dg;
-    dgp[cm.C + c] = db;
+  if (dgb) {
+    float* dgp = dgb + (long long)l * dgb_ls;
+    if (accumulate) {
+      dgp[c] += dg;
+      dgp[cm.C + c] += db;
+    } else {
+      dgp[c] = dg;
+      dgp[cm.C + c] = db;
+    }
   }
   if (dbias) {
     // sum over rows of gz, in closed form from the channel sums
@@ -300,15 +302,17 @@ __global__ void adam_tick_kernel(int L, const int* flags, long long* t) {
 }
 
 __global__ void adam_kernel(long long P, float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
-                            float* __restrict__ v, const long long* t, const int* flags, float lr, float b1, float b2,
-                            float eps) {
+                            float* __restrict__ v, const long long* t, const int* flags, float lr, double b1d,
+                            double b2d, float eps) {
   const int l = blockIdx.y;
   if (flags[l]) return;  // rejected step: state untouched (optim.cpp:25)
+  const float b1 = (float)b1d, b2 = (float)b2d;
   __shared__ float c12[2];
   if (threadIdx.x == 0) {
+    // bias corrections from the f64 betas, as std::pow in optim.cpp:30-31
     double tt = (double)t[l];
-    c12[0] = (float)(1.0 - pow((double)b1, tt));
-    c12[1] = (float)(1.0 - pow((double)b2, tt));
+    c12[0] = (float)(1.0 - pow(b1d, tt));
+    c12[1] = (float)(1.0 - pow(b2d, tt));
   }
   __syncthreads();
   const float c1 = c12[0], c2 = c12[1];
@@ -494,7 +498,7 @@ cudaError_t launch_adam_tick(int L, const int* flags, long long* t, cudaStream_t
 }
 
 cudaError_t launch_adam(int L, long long P, float* params, const float* grads, float* m, float* v,
-                        const long long* t, const int* flags, float lr, float b1, float b2, float eps,
+                        const long long* t, const int* flags, float lr, double b1, double b2, float eps,
                         cudaStream_t st) {
   dim3 grid(grid_for(P / 4, 256, 256), L);
   adam_kernel<<<grid, 256, 0, st>>>(P, params, grads, m, v, t, flags, lr, b1, b2, eps);

@@ -213,7 +213,7 @@ void GanGroup::enqueue_step(int B, const float* real_nhwc, int par) {
   check_cuda(launch_nonfinite_check(L_, D_->P(), D_->grads.p, d_flags_, st_), "nonfinite D");
   check_cuda(launch_adam_tick(L_, d_flags_, d_t_d_, st_), "tick D");
   check_cuda(launch_adam(L_, D_->P(), D_->params.p, D_->grads.p, D_->adam_m.p, D_->adam_v.p, d_t_d_, d_flags_,
-                         static_cast<float>(cfg_.lr), static_cast<float>(cfg_.beta1), static_cast<float>(cfg_.beta2),
+                         static_cast<float>(cfg_.lr), cfg_.beta1, cfg_.beta2,
                          static_cast<float>(cfg_.eps), st_),
              "adam D");
   // generator update through the updated discriminator (its grads discarded)
@@ -228,7 +228,7 @@ void GanGroup::enqueue_step(int B, const float* real_nhwc, int par) {
   check_cuda(launch_nonfinite_check(L_, G_->P(), G_->grads.p, d_flags_, st_), "nonfinite G");
   check_cuda(launch_adam_tick(L_, d_flags_, d_t_g_, st_), "tick G");
   check_cuda(launch_adam(L_, G_->P(), G_->params.p, G_->grads.p, G_->adam_m.p, G_->adam_v.p, d_t_g_, d_flags_,
-                         static_cast<float>(cfg_.lr), static_cast<float>(cfg_.beta1), static_cast<float>(cfg_.beta2),
+                         static_cast<float>(cfg_.lr), cfg_.beta1, cfg_.beta2,
                          static_cast<float>(cfg_.eps), st_),
              "adam G");
   steps_ += 1;

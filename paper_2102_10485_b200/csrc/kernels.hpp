@@ -80,7 +80,7 @@ cudaError_t launch_loss_g(int L, int B, const float* p_fake, int pstride, double
 cudaError_t launch_nonfinite_check(int L, long long P, const float* grads, int* flags, cudaStream_t st);
 cudaError_t launch_adam_tick(int L, const int* flags, long long* t, cudaStream_t st);
 cudaError_t launch_adam(int L, long long P, float* params, const float* grads, float* m, float* v,
-                        const long long* t, const int* flags, float lr, float b1, float b2, float eps,
+                        const long long* t, const int* flags, float lr, double b1, double b2, float eps,
                         cudaStream_t st);
 
 // ---- data movement ----

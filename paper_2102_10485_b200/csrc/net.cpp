@@ -3,13 +3,19 @@
 #include "net.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <sstream>
 
 #include "rng.hpp"
 
 namespace pg {
 
+// PG_DEBUG_SYNC=1: synchronize after every checked call so an asynchronous
+// fault is attributed to the launch that caused it.
+static const bool g_debug_sync = std::getenv("PG_DEBUG_SYNC") != nullptr;
+
 void check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess && g_debug_sync) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
