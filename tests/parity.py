@@ -69,8 +69,10 @@ def layer_tensors(spec: str, in_shape: tuple) -> list[tuple[str, int, int, bool]
     items = [t.split() for t in spec.split(";") if t.split()]
     out, off = [], 0
     for i, tok in enumerate(items):
-        nxt = [t[0] for t in items[i + 1:i + 3]]
-        feeds_bn = "bn" in nxt[:1] or (nxt[:1] == ["reshape"] and "bn" in nxt[1:2])
+        nxt = [t[0] for t in items[i + 1:i + 2]]
+        # a per-channel bias directly before BatchNorm is a gauge direction; a
+        # dense bias reshaped to [C,H,W] is per position and is not
+        feeds_bn = nxt == ["bn"]
         if tok[0] == "dense":
             a, b = int(tok[1]), int(tok[2])
             out += [(f"{i}.dense.w", off, a * b, False), (f"{i}.dense.b", off + a * b, b, feeds_bn)]

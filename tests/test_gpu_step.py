@@ -81,8 +81,10 @@ def test_single_step_parity(oracle, cfg, n_labels, per_label, batch, math):
     assert grp.train_steps(1) == 1
     orc.step(1)
     for l in range(n_labels):
-        # minibatch indices: bit-exact
-        assert np.array_equal(grp.get(l, N.F_LAST_BATCH), orc.get(l, OR["batch"]))
+        # minibatch indices: bit-exact.  The device group reports positions in
+        # the label's shard; the oracle reports rows of its label-blocked
+        # dataset (row = l * per_label + position).
+        assert np.array_equal(grp.get(l, N.F_LAST_BATCH) + l * per_label, orc.get(l, OR["batch"]))
         r, q = grp.reports(l)[-1], orc.get(l, OR["reports"]).reshape(-1, 4)[-1]
         assert abs(r[0] - q[0]) <= 1e-4 * abs(q[0]), (r, q)   # J_D
         assert abs(r[1] - q[1]) <= 1e-4 * abs(q[1]), (r, q)   # J_G
@@ -103,7 +105,8 @@ def test_ten_step_trajectory_and_ragged_tail(oracle):
             assert grp.train_steps(1) == 1
             orc.step(1)
             for l in range(2):
-                assert np.array_equal(grp.get(l, N.F_LAST_BATCH), orc.get(l, OR["batch"])), (per_label, s)
+                assert np.array_equal(grp.get(l, N.F_LAST_BATCH) + l * per_label, orc.get(l, OR["batch"])), \
+                    (per_label, s)
         for l in range(2):
             r = grp.reports(l)
             q = orc.get(l, OR["reports"]).reshape(-1, 4)
