@@ -15,11 +15,11 @@
 // Operand layouts in shared memory (SWIZZLE_NONE canonical forms):
 //   K-major  (contiguous K in global):  16-byte chunk c of row r at
 //            c*(R*16) + (r/8)*128 + (r%8)*16;  LBO = R*16, SBO = 128.
-//   MN-major (contiguous M/N in global): 4 MN-elements x 1 k per 16 bytes at
-//            (k/8)*LBO + (mn/4)*144 + (k%8)*16; SBO = 144 (16 bytes of pad per
-//            core matrix keeps warp-wide 16-byte stores bank-conflict free),
-//            LBO = (R/4)*144.
+//   MN-major (contiguous M/N in global): the only layout tcgen05 accepts for
+//            tf32 MN-major operands is SWIZZLE_128B_BASE32B (see mn_offset).
 #include <stdint.h>
+
+#include <cstdlib>
 
 #include "gemm_gather.cuh"
 #include "kernels.hpp"
@@ -31,7 +31,15 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 32;          // fp32 elements of K per stage
 constexpr int NPROD = 128;      // producer / epilogue threads
-constexpr int MN_SBO = 144;
+// MN-major tf32 operands must use the 128B swizzle with 32-byte atoms
+// (descriptor layout type 1, "SWIZZLE_128B_BASE32B"): an atom is 32 MN
+// elements (128 B) x 4 K rows (128 B apart), 16-byte chunk bits [5,7) of the
+// address XORed with the row bits [7,9).  Atoms: MN-adjacent at 512 B (LBO),
+// K-adjacent at (R/32)*512 B (SBO).
+PG_DEV int mn_offset(int R, int col4, int kr) {
+  const int row = kr & 3;
+  return (kr >> 2) * ((R / 32) * 512) + (col4 >> 3) * 512 + row * 128 + (((col4 & 7) * 16) ^ (row << 5));
+}
 
 // ---- PTX wrappers -------------------------------------------------------
 PG_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -87,9 +95,9 @@ PG_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 PG_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // SWIZZLE_NONE shared-memory matrix descriptor (version 1 = tcgen05)
-PG_DEV uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+PG_DEV uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
 }
 
 // kind::tf32 instruction descriptor: D f32, A/B tf32, M = 128, N = BN
@@ -100,7 +108,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int bn, bool a_mn, bool b_mn) 
 
 // ---- tile geometry ------------------------------------------------------
 __host__ __device__ constexpr int kmajor_bytes(int rows) { return rows * BK * 4; }
-__host__ __device__ constexpr int mnmajor_bytes(int rows) { return (BK / 8) * (rows / 4) * MN_SBO; }
+__host__ __device__ constexpr int mnmajor_bytes(int rows) { return rows * BK * 4; }  // rows % 32 == 0
 __host__ __device__ constexpr bool a_is_mn(int kind) { return kind == GEMM_WGRAD; }
 __host__ __device__ constexpr bool b_is_mn(int kind) { return kind != GEMM_FPROP; }
 __host__ __device__ constexpr int a_tile_bytes(int kind) { return a_is_mn(kind) ? mnmajor_bytes(BM) : kmajor_bytes(BM); }
@@ -227,6 +235,11 @@ __global__ void __launch_bounds__(NPROD + 32, 1) gemm_tc_kernel(GemmArgs a) {
   if (warp == 4) {
     // ===================== MMA issuer =====================
     constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN);
+    // one K=8 MMA spans two K-chunks (K-major) or two 4-row K atoms (MN-major)
+    constexpr uint32_t alb = A_MN ? 512u : BM * 16u, asb = A_MN ? (BM / 32) * 512u : 128u;
+    constexpr uint32_t blb = B_MN ? 512u : BN * 16u, bsb = B_MN ? (BN / 32) * 512u : 128u;
+    constexpr uint32_t astep = A_MN ? 2 * asb : 2 * alb, bstep = B_MN ? 2 * bsb : 2 * blb;
+    constexpr uint32_t alay = A_MN ? 1u : 0u, blay = B_MN ? 1u : 0u;
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % STAGES;
       mbar_wait(full + s, (kb / STAGES) & 1);
@@ -238,21 +251,11 @@ __global__ void __launch_bounds__(NPROD + 32, 1) gemm_tc_kernel(GemmArgs a) {
         const uint32_t b_lo = a_lo + A_BYTES;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          uint32_t aoff, boff, alb, asb, blb, bsb;
-          if (A_MN) {
-            alb = (BM / 4) * MN_SBO; asb = MN_SBO; aoff = kk * alb;
-          } else {
-            alb = BM * 16; asb = 128; aoff = 2 * kk * alb;
-          }
-          if (B_MN) {
-            blb = (BN / 4) * MN_SBO; bsb = MN_SBO; boff = kk * blb;
-          } else {
-            blb = BN * 16; bsb = 128; boff = 2 * kk * blb;
-          }
-          const uint64_t ah = make_desc(a_hi + aoff, alb, asb), bh = make_desc(b_hi + boff, blb, bsb);
+          const uint32_t aoff = kk * astep, boff = kk * bstep;
+          const uint64_t ah = make_desc(a_hi + aoff, alb, asb, alay), bh = make_desc(b_hi + boff, blb, bsb, blay);
           const uint32_t acc = (kb | kk) ? 1u : 0u;
           if (SPLIT) {
-            const uint64_t al = make_desc(a_lo + aoff, alb, asb), bl = make_desc(b_lo + boff, blb, bsb);
+            const uint64_t al = make_desc(a_lo + aoff, alb, asb, alay), bl = make_desc(b_lo + boff, blb, bsb, blay);
             mma_tf32(tmem, al, bh, idesc, acc);  // small terms first
             mma_tf32(tmem, ah, bl, idesc, 1u);
             mma_tf32(tmem, ah, bh, idesc, 1u);
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(NPROD + 32, 1) gemm_tc_kernel(GemmArgs a) {
         for (int j = 0; j < BK / 4; ++j) {
           const int kr = krow0 + 4 * j, k = k0 + kr, m = m0 + 4 * mn4;
           const float* p = (k < v.K && m < v.M) ? v.A + (long long)k * g.CS + m : nullptr;
-          put4<SPLIT>(a_hi, a_lo, (kr / 8) * ((BM / 4) * MN_SBO) + mn4 * MN_SBO + (kr % 8) * 16, ld4(p));
+          put4<SPLIT>(a_hi, a_lo, mn_offset(BM, mn4, kr), ld4(p));
         }
       }
       // ---------------- B ----------------
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(NPROD + 32, 1) gemm_tc_kernel(GemmArgs a) {
               if (KIND == GEMM_DGRAD) p = dgrad_b_ptr(g, v, n, k);
               else p = wgrad_b_ptr(g, v, n, k);
             }
-            put4<SPLIT>(b_hi, b_lo, (kr / 8) * (COLS * MN_SBO) + col * MN_SBO + (kr % 8) * 16, ld4(p));
+            put4<SPLIT>(b_hi, b_lo, mn_offset(BN, col, kr), ld4(p));
           }
         }
       }
@@ -416,7 +419,8 @@ cudaError_t launch_bn(const GemmArgs& a, cudaStream_t st) {
 template <int KIND, int MODE>
 cudaError_t launch_kind(const GemmArgs& a, cudaStream_t st) {
   const int n = gemm_n(a);
-  if (n <= 16) return launch_bn<KIND, 16, MODE>(a, st);
+  // MN-major B tiles (DGRAD / WGRAD) are built from 32-element swizzle atoms
+  if (KIND == GEMM_FPROP && n <= 16) return launch_bn<KIND, 16, MODE>(a, st);
   if (n <= 32) return launch_bn<KIND, 32, MODE>(a, st);
   if (n <= 64) return launch_bn<KIND, 64, MODE>(a, st);
   return launch_bn<KIND, 128, MODE>(a, st);
