@@ -1,25 +1,34 @@
 // tcgen05 implicit-GEMM engine (sm_100a): math modes TF32 (one kind::tf32
 // MMA per K-step) and TF32X3 (split a = a_hi + a_lo, b = b_hi + b_lo in
-// shared memory; D += a_hi b_hi + a_hi b_lo + a_lo b_hi, fp32-accurate).
+// shared memory; D += a_lo b_hi + a_hi b_lo + a_hi b_hi, fp32-accurate).
 //
-// One CTA computes a 128 x BN tile of one (label, phase) problem:
+// Persistent, warp-specialized; each CTA walks 128 x BN output tiles of the
+// (label, phase) problems in a static round-robin:
 //   warps 0-3  producers: gather the A / B tiles straight from the NHWC maps
-//              (the implicit-GEMM index maps of gemm_gather.cuh, with the
-//              per-row state hoisted out of the K loop), split hi/lo, write
-//              the UMMA canonical no-swizzle layouts, arrive on full[stage];
-//              after the K loop the same warps are the epilogue: tcgen05.ld
-//              the fp32 accumulator from TMEM, bias + activation, store.
-//   warp 4     TMEM allocation + the single MMA-issuing thread: waits
-//              full[stage], issues the MMAs, tcgen05.commit -> empty[stage];
-//              a final commit -> accum signals the epilogue.
-// Operand layouts in shared memory (SWIZZLE_NONE canonical forms):
-//   K-major  (contiguous K in global):  16-byte chunk c of row r at
-//            c*(R*16) + (r/8)*128 + (r%8)*16;  LBO = R*16, SBO = 128.
-//   MN-major (contiguous M/N in global): the only layout tcgen05 accepts for
-//            tf32 MN-major operands is SWIZZLE_128B_BASE32B (see mn_offset).
+//              (implicit-GEMM index maps of gemm_gather.cuh with the per-row
+//              state hoisted out of the K loop), split hi/lo, write the UMMA
+//              canonical layouts, arrive on full[stage].
+//   warp 4     the single MMA-issuing thread (and TMEM allocation): K is cut
+//              into segments of KSEG k-blocks; each segment accumulates into
+//              one of two TMEM buffers (ping-pong) and is committed to
+//              seg_full[buf].
+//   warps 5-8  drain + epilogue: each segment is pulled out of TMEM
+//              (tcgen05.ld) and added into an IEEE fp32 running sum in
+//              registers, then the buffer is released (seg_empty[buf]).
+//              After the last segment of a tile: bias + activation, store.
+// Why drain: the tensor core accumulates with truncation, so one TMEM
+// accumulator over K = 16384 loses ~1e-4 relative; segments of 2 k-blocks
+// keep every accumulation chain at <= 24 MMA adds, which brings 3xTF32 to
+// the accuracy of a plain fp32 FMA loop (scripts/tc_accuracy.py).
+//
+// Shared-memory operand layouts:
+//   K-major  (contiguous K in global), SWIZZLE_NONE: 16-byte chunk c of row r
+//            at c*(R*16) + (r/8)*128 + (r%8)*16; LBO = R*16, SBO = 128.
+//   MN-major (contiguous M/N in global): tcgen05 accepts tf32 MN-major
+//            operands only in SWIZZLE_128B_BASE32B (see mn_offset).
 #include <stdint.h>
 
-#include <cstdlib>
+#include <algorithm>
 
 #include "gemm_gather.cuh"
 #include "kernels.hpp"
@@ -30,12 +39,14 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;          // fp32 elements of K per stage
-constexpr int NPROD = 128;      // producer / epilogue threads
-// MN-major tf32 operands must use the 128B swizzle with 32-byte atoms
-// (descriptor layout type 1, "SWIZZLE_128B_BASE32B"): an atom is 32 MN
-// elements (128 B) x 4 K rows (128 B apart), 16-byte chunk bits [5,7) of the
-// address XORed with the row bits [7,9).  Atoms: MN-adjacent at 512 B (LBO),
-// K-adjacent at (R/32)*512 B (SBO).
+constexpr int NPROD = 128;      // warps 0-3
+constexpr int NDRAIN = 128;     // warps 5-8
+constexpr int NTHREADS = NPROD + 32 + NDRAIN;
+constexpr int KSEG = 2;         // k-blocks per TMEM accumulation segment
+
+// MN-major atom: 32 MN elements (128 B) x 4 K rows (128 B apart); the 16-byte
+// chunk bits [5,7) are XORed with the row bits [7,9).  Atoms MN-adjacent at
+// 512 B (LBO), K-adjacent at (R/32)*512 B (SBO).
 PG_DEV int mn_offset(int R, int col4, int kr) {
   const int row = kr & 3;
   return (kr >> 2) * ((R / 32) * 512) + (col4 >> 3) * 512 + row * 128 + (((col4 & 7) * 16) ^ (row << 5));
@@ -94,7 +105,7 @@ PG_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 PG_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// SWIZZLE_NONE shared-memory matrix descriptor (version 1 = tcgen05)
+// shared-memory matrix descriptor (version 1 = tcgen05); layout 0 = none, 1 = 128B_BASE32B
 PG_DEV uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
@@ -107,23 +118,19 @@ __host__ __device__ constexpr uint32_t make_idesc(int bn, bool a_mn, bool b_mn) 
 }
 
 // ---- tile geometry ------------------------------------------------------
-__host__ __device__ constexpr int kmajor_bytes(int rows) { return rows * BK * 4; }
-__host__ __device__ constexpr int mnmajor_bytes(int rows) { return rows * BK * 4; }  // rows % 32 == 0
+__host__ __device__ constexpr int tile_bytes(int rows) { return rows * BK * 4; }
 __host__ __device__ constexpr bool a_is_mn(int kind) { return kind == GEMM_WGRAD; }
 __host__ __device__ constexpr bool b_is_mn(int kind) { return kind != GEMM_FPROP; }
-__host__ __device__ constexpr int a_tile_bytes(int kind) { return a_is_mn(kind) ? mnmajor_bytes(BM) : kmajor_bytes(BM); }
-__host__ __device__ constexpr int b_tile_bytes(int kind, int bn) {
-  return b_is_mn(kind) ? mnmajor_bytes(bn) : kmajor_bytes(bn);
+__host__ __device__ constexpr int stage_bytes(int bn, bool split) {
+  return (tile_bytes(BM) + tile_bytes(bn)) * (split ? 2 : 1);
 }
-__host__ __device__ constexpr int stage_bytes(int kind, int bn, bool split) {
-  return (a_tile_bytes(kind) + b_tile_bytes(kind, bn)) * (split ? 2 : 1);
+__host__ __device__ constexpr int num_stages(int bn, bool split) {
+  return stage_bytes(bn, split) * 4 <= 192 * 1024 ? 4 : (stage_bytes(bn, split) * 3 <= 192 * 1024 ? 3 : 2);
 }
-__host__ __device__ constexpr int num_stages(int kind, int bn, bool split) {
-  return stage_bytes(kind, bn, split) * 4 <= 200 * 1024 ? 4 : (stage_bytes(kind, bn, split) * 3 <= 200 * 1024 ? 3 : 2);
+__host__ __device__ constexpr int smem_bytes(int bn, bool split) {
+  return num_stages(bn, split) * stage_bytes(bn, split) + 1024 /* barriers */ + 1024 /* alignment */;
 }
-__host__ __device__ constexpr int smem_total(int kind, int bn, bool split) {
-  return num_stages(kind, bn, split) * stage_bytes(kind, bn, split) + 1024 /* barriers + align */;
-}
+__host__ __device__ constexpr uint32_t tmem_cols(int bn) { return 2 * bn <= 32 ? 32 : 2 * bn; }
 
 PG_DEV float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
@@ -152,10 +159,8 @@ template <int KIND>
 PG_DEV RowState row_state(const ConvGeo& g, const GemmView& v, int m) {
   RowState r;
   r.valid = m < v.M;
-  if (!r.valid) {
-    r.b = r.y0 = r.x0 = 0;
-    return r;
-  }
+  r.b = r.y0 = r.x0 = 0;
+  if (!r.valid) return r;
   if (KIND == GEMM_FPROP) {
     int j = m % g.SW, t = m / g.SW;
     int i = t % g.SH;
@@ -192,38 +197,49 @@ PG_DEV const float* a_row_ptr(const ConvGeo& g, const GemmView& v, const RowStat
   }
 }
 
+struct TileGrid {
+  int ntn, ntm, nz;  // n tiles, m tiles (max over phases), labels x phases
+  __host__ __device__ int total() const { return ntn * ntm * nz; }
+};
+
+PG_DEV void tile_coords(const TileGrid& tg, int t, int& z, int& mt, int& nt) {
+  nt = t % tg.ntn;
+  const int r = t / tg.ntn;
+  mt = r % tg.ntm;
+  z = r / tg.ntm;
+}
+
 template <int KIND, int BN, int MODE>
-__global__ void __launch_bounds__(NPROD + 32, 1) gemm_tc_kernel(GemmArgs a) {
+__global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(GemmArgs a, TileGrid tg) {
   constexpr bool SPLIT = MODE == MATH_TF32X3;
-  constexpr int STAGES = num_stages(KIND, BN, SPLIT);
-  constexpr int A_BYTES = a_tile_bytes(KIND);
-  constexpr int B_BYTES = b_tile_bytes(KIND, BN);
-  constexpr int STAGE = stage_bytes(KIND, BN, SPLIT);
+  constexpr int STAGES = num_stages(BN, SPLIT);
+  constexpr int A_BYTES = tile_bytes(BM);
+  constexpr int B_BYTES = tile_bytes(BN);
+  constexpr int STAGE = stage_bytes(BN, SPLIT);
   constexpr bool A_MN = a_is_mn(KIND), B_MN = b_is_mn(KIND);
-  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN;
+  constexpr uint32_t TMEM_COLS = tmem_cols(BN);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
-  uint64_t* accum = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* seg_full = empty + STAGES;
+  uint64_t* seg_empty = seg_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(seg_empty + 2);
 
-  const int phases = gemm_phases(a);
-  const int label = blockIdx.z / phases, phase = blockIdx.z % phases;
-  const GemmView v = make_view(a, label, phase);
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  if (m0 >= v.M || n0 >= v.N) return;  // uniform per CTA
-  const ConvGeo& g = a.g;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  const int nk = (v.K + BK - 1) / BK;
+  const int phases = gemm_phases(a);
+  const ConvGeo& g = a.g;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, NPROD);
       mbar_init(empty + s, 1);
     }
-    mbar_init(accum, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(seg_full + b, 1);
+      mbar_init(seg_empty + b, NDRAIN);
+    }
     fence_barrier_init();
   }
   if (warp == 4) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -232,163 +248,208 @@ __global__ void __launch_bounds__(NPROD + 32, 1) gemm_tc_kernel(GemmArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
-    // ===================== MMA issuer =====================
-    constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN);
-    // one K=8 MMA spans two K-chunks (K-major) or two 4-row K atoms (MN-major)
-    constexpr uint32_t alb = A_MN ? 512u : BM * 16u, asb = A_MN ? (BM / 32) * 512u : 128u;
-    constexpr uint32_t blb = B_MN ? 512u : BN * 16u, bsb = B_MN ? (BN / 32) * 512u : 128u;
-    constexpr uint32_t astep = A_MN ? 2 * asb : 2 * alb, bstep = B_MN ? 2 * bsb : 2 * blb;
-    constexpr uint32_t alay = A_MN ? 1u : 0u, blay = B_MN ? 1u : 0u;
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(full + s, (kb / STAGES) & 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t a_hi = smem_u32(smem + s * STAGE);
-        const uint32_t b_hi = a_hi + A_BYTES;
-        const uint32_t a_lo = a_hi + A_BYTES + B_BYTES;
-        const uint32_t b_lo = a_lo + A_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint32_t aoff = kk * astep, boff = kk * bstep;
-          const uint64_t ah = make_desc(a_hi + aoff, alb, asb, alay), bh = make_desc(b_hi + boff, blb, bsb, blay);
-          const uint32_t acc = (kb | kk) ? 1u : 0u;
-          if (SPLIT) {
-            const uint64_t al = make_desc(a_lo + aoff, alb, asb, alay), bl = make_desc(b_lo + boff, blb, bsb, blay);
-            mma_tf32(tmem, al, bh, idesc, acc);  // small terms first
-            mma_tf32(tmem, ah, bl, idesc, 1u);
-            mma_tf32(tmem, ah, bh, idesc, 1u);
-          } else {
-            mma_tf32(tmem, ah, bh, idesc, acc);
-          }
-        }
-        mma_commit(empty + s);                 // frees the stage when these MMAs retire
-        if (kb == nk - 1) mma_commit(accum);   // accumulator complete
-      }
-      __syncwarp();
-    }
-    if (nk == 0 && lane == 0) mbar_arrive(accum);
-  } else {
+  uint32_t kc = 0;  // k-blocks consumed / produced so far (stage ring)
+  uint32_t sc = 0;  // segments so far (TMEM ping-pong)
+  const int ntiles = tg.total();
+
+  if (warp < 4) {
     // ===================== producers =====================
-    RowState rs = row_state<KIND>(g, v, m0 + tid);  // A row of this thread (K-major A)
-    // MN-major operands: fixed 16-byte column per thread, k rows tid/32 + 4j
-    const int mn4 = tid % 32;
-    const int krow0 = tid / 32;
-    // WGRAD B: fixed (tap, cg) per thread and N sub-block
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(empty + s, ((kb / STAGES) & 1) ^ 1);
-      uint8_t* a_hi = smem + s * STAGE;
-      uint8_t* b_hi = a_hi + A_BYTES;
-      uint8_t* a_lo = a_hi + A_BYTES + B_BYTES;
-      uint8_t* b_lo = a_lo + A_BYTES;
-      const int k0 = kb * BK;
-      // ---------------- A ----------------
-      if (!A_MN) {
-        // 128 rows x 8 chunks; this thread owns row tid
-        const bool one_tap = (KIND == GEMM_FPROP ? g.CG : g.CS) % BK == 0;
-        if (one_tap) {
-          const float* base = a_row_ptr<KIND>(g, v, rs, k0);
+    const int mn4 = tid % 32, krow0 = tid / 32;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int z, mt, nt;
+      tile_coords(tg, t, z, mt, nt);
+      const GemmView v = make_view(a, z / phases, z % phases);
+      const int m0 = mt * BM, n0 = nt * BN;
+      if (m0 >= v.M || n0 >= v.N) continue;
+      const int nk = (v.K + BK - 1) / BK;
+      const RowState rs = row_state<KIND>(g, v, m0 + tid);
+      const bool one_tap = (KIND == GEMM_FPROP ? g.CG : g.CS) % BK == 0;
+      for (int kb = 0; kb < nk; ++kb, ++kc) {
+        const int s = kc % STAGES;
+        mbar_wait(empty + s, ((kc / STAGES) & 1) ^ 1);
+        uint8_t* a_hi = smem + s * STAGE;
+        uint8_t* b_hi = a_hi + A_BYTES;
+        uint8_t* a_lo = b_hi + B_BYTES;
+        uint8_t* b_lo = a_lo + A_BYTES;
+        const int k0 = kb * BK;
+        // ---------------- A ----------------
+        if (!A_MN) {
+          // 128 rows x 8 chunks; this thread owns row tid
+          if (one_tap) {
+            const float* base = a_row_ptr<KIND>(g, v, rs, k0);
 #pragma unroll
-          for (int c = 0; c < BK / 4; ++c) {
-            const float* p = (base && k0 + 4 * c < v.K) ? base + 4 * c : nullptr;
-            put4<SPLIT>(a_hi, a_lo, c * (BM * 16) + (tid / 8) * 128 + (tid % 8) * 16, ld4(p));
+            for (int c = 0; c < BK / 4; ++c) {
+              const float* p = (base && k0 + 4 * c < v.K) ? base + 4 * c : nullptr;
+              put4<SPLIT>(a_hi, a_lo, c * (BM * 16) + (tid / 8) * 128 + (tid % 8) * 16, ld4(p));
+            }
+          } else {
+#pragma unroll 2
+            for (int c = 0; c < BK / 4; ++c) {
+              const float* p = a_row_ptr<KIND>(g, v, rs, k0 + 4 * c);
+              put4<SPLIT>(a_hi, a_lo, c * (BM * 16) + (tid / 8) * 128 + (tid % 8) * 16, ld4(p));
+            }
           }
         } else {
-#pragma unroll 2
-          for (int c = 0; c < BK / 4; ++c) {
-            const float* p = a_row_ptr<KIND>(g, v, rs, k0 + 4 * c);
-            put4<SPLIT>(a_hi, a_lo, c * (BM * 16) + (tid / 8) * 128 + (tid % 8) * 16, ld4(p));
+          // WGRAD A[m = cs][k = spix] = smallg[spix][cs]: 32 float4 columns x 32 k rows
+#pragma unroll
+          for (int j = 0; j < BK / 4; ++j) {
+            const int kr = krow0 + 4 * j, k = k0 + kr, m = m0 + 4 * mn4;
+            const float* p = (k < v.K && m < v.M) ? v.A + (long long)k * g.CS + m : nullptr;
+            put4<SPLIT>(a_hi, a_lo, mn_offset(BM, mn4, kr), ld4(p));
           }
         }
-      } else {
-        // WGRAD A[m = cs][k = spix] = smallg[spix][cs]: 32 float4 columns x 32 k rows
+        // ---------------- B ----------------
+        if (!B_MN) {
+          // FPROP: B[n][k] = W[n][k], rows contiguous over K; BN rows x 8 chunks
 #pragma unroll
-        for (int j = 0; j < BK / 4; ++j) {
-          const int kr = krow0 + 4 * j, k = k0 + kr, m = m0 + 4 * mn4;
-          const float* p = (k < v.K && m < v.M) ? v.A + (long long)k * g.CS + m : nullptr;
-          put4<SPLIT>(a_hi, a_lo, mn_offset(BM, mn4, kr), ld4(p));
+          for (int it = 0; it < (BN * (BK / 4) + NPROD - 1) / NPROD; ++it) {
+            const int item = tid + it * NPROD;
+            if (item < BN * (BK / 4)) {
+              const int c = item / BN, r = item % BN;
+              const int n = n0 + r, k = k0 + 4 * c;
+              const float* p = (n < v.N && k < v.K) ? v.Bw + (long long)n * v.K + k : nullptr;
+              put4<SPLIT>(b_hi, b_lo, c * (BN * 16) + (r / 8) * 128 + (r % 8) * 16, ld4(p));
+            }
+          }
+        } else {
+          // MN-major B: (BN/4) float4 columns x 32 k rows
+          constexpr int COLS = BN / 4;
+          constexpr int ITEMS = COLS * BK;
+#pragma unroll
+          for (int it = 0; it < (ITEMS + NPROD - 1) / NPROD; ++it) {
+            const int item = tid + it * NPROD;
+            if (item < ITEMS) {
+              const int col = item % COLS, kr = item / COLS;
+              const int n = n0 + 4 * col, k = k0 + kr;
+              const float* p = nullptr;
+              if (n < v.N && k < v.K) {
+                if (KIND == GEMM_DGRAD) p = dgrad_b_ptr(g, v, n, k);
+                else p = wgrad_b_ptr(g, v, n, k);
+              }
+              put4<SPLIT>(b_hi, b_lo, mn_offset(BN, col, kr), ld4(p));
+            }
+          }
+        }
+        fence_async_smem();
+        mbar_arrive(full + s);
+      }
+    }
+  } else if (warp == 4) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN);
+      // one K=8 MMA spans two K-chunks (K-major) or two 4-row K atoms (MN-major)
+      constexpr uint32_t alb = A_MN ? 512u : BM * 16u, asb = A_MN ? (BM / 32) * 512u : 128u;
+      constexpr uint32_t blb = B_MN ? 512u : BN * 16u, bsb = B_MN ? (BN / 32) * 512u : 128u;
+      constexpr uint32_t astep = A_MN ? 2 * asb : 2 * alb, bstep = B_MN ? 2 * bsb : 2 * blb;
+      constexpr uint32_t alay = A_MN ? 1u : 0u, blay = B_MN ? 1u : 0u;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int z, mt, nt;
+        tile_coords(tg, t, z, mt, nt);
+        const GemmView v = make_view(a, z / phases, z % phases);
+        if (mt * BM >= v.M || nt * BN >= v.N) continue;
+        const int nk = (v.K + BK - 1) / BK;
+        for (int k_seg = 0; k_seg < nk; k_seg += KSEG, ++sc) {
+          const uint32_t buf = sc & 1;
+          mbar_wait(seg_empty + buf, ((sc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + buf * BN;
+          const int k_end = min(nk, k_seg + KSEG);
+          for (int kb = k_seg; kb < k_end; ++kb, ++kc) {
+            const int s = kc % STAGES;
+            mbar_wait(full + s, (kc / STAGES) & 1);
+            tc_fence_after();
+            const uint32_t a_hi = smem_u32(smem + s * STAGE);
+            const uint32_t b_hi = a_hi + A_BYTES;
+            const uint32_t a_lo = b_hi + B_BYTES;
+            const uint32_t b_lo = a_lo + A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t ah = make_desc(a_hi + kk * astep, alb, asb, alay);
+              const uint64_t bh = make_desc(b_hi + kk * bstep, blb, bsb, blay);
+              const uint32_t acc = (kb != k_seg || kk) ? 1u : 0u;
+              if (SPLIT) {
+                const uint64_t al = make_desc(a_lo + kk * astep, alb, asb, alay);
+                const uint64_t bl = make_desc(b_lo + kk * bstep, blb, bsb, blay);
+                mma_tf32(d, al, bh, idesc, acc);  // small terms first
+                mma_tf32(d, ah, bl, idesc, 1u);
+                mma_tf32(d, ah, bh, idesc, 1u);
+              } else {
+                mma_tf32(d, ah, bh, idesc, acc);
+              }
+            }
+            mma_commit(empty + s);  // frees the stage when these MMAs retire
+          }
+          mma_commit(seg_full + buf);  // segment accumulated
         }
       }
-      // ---------------- B ----------------
-      if (!B_MN) {
-        // FPROP: B[n][k] = W[n][k], rows contiguous over K; BN rows x 8 chunks
+    }
+    __syncwarp();
+  } else {
+    // ===================== drain + epilogue =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int z, mt, nt;
+      tile_coords(tg, t, z, mt, nt);
+      const GemmView v = make_view(a, z / phases, z % phases);
+      const int m0 = mt * BM, n0 = nt * BN;
+      if (m0 >= v.M || n0 >= v.N) continue;
+      const int nk = (v.K + BK - 1) / BK;
+      float acc[BN];
 #pragma unroll
-        for (int it = 0; it < (BN * (BK / 4) + NPROD - 1) / NPROD; ++it) {
-          const int item = tid + it * NPROD;
-          if (item < BN * (BK / 4)) {
-            const int c = item / BN, r = item % BN;
-            const int n = n0 + r, k = k0 + 4 * c;
-            const float* p = (n < v.N && k < v.K) ? v.Bw + (long long)n * v.K + k : nullptr;
-            put4<SPLIT>(b_hi, b_lo, c * (BN * 16) + (r / 8) * 128 + (r % 8) * 16, ld4(p));
-          }
-        }
-      } else {
-        // MN-major B: (BN/4) float4 columns x 32 k rows
-        constexpr int COLS = BN / 4;
-        constexpr int ITEMS = COLS * BK;
+      for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+      for (int k_seg = 0; k_seg < nk; k_seg += KSEG, ++sc) {
+        const uint32_t buf = sc & 1;
+        mbar_wait(seg_full + buf, (sc >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
-        for (int it = 0; it < (ITEMS + NPROD - 1) / NPROD; ++it) {
-          const int item = tid + it * NPROD;
-          if (item < ITEMS) {
-            const int col = item % COLS, kr = item / COLS;
-            const int n = n0 + 4 * col, k = k0 + kr;
-            const float* p = nullptr;
-            if (n < v.N && k < v.K) {
-              if (KIND == GEMM_DGRAD) p = dgrad_b_ptr(g, v, n, k);
-              else p = wgrad_b_ptr(g, v, n, k);
-            }
-            put4<SPLIT>(b_hi, b_lo, mn_offset(BN, col, kr), ld4(p));
-          }
+        for (int c = 0; c < BN / 16; ++c) {
+          uint32_t r[16];
+          tmem_ld16(tmem + lane_base + buf * BN + c * 16, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[c * 16 + i] += __uint_as_float(r[i]);
         }
+        tc_fence_before();
+        mbar_arrive(seg_empty + buf);
       }
-      fence_async_smem();
-      mbar_arrive(full + s);
-    }
-
-    // ===================== epilogue =====================
-    mbar_wait(accum, 0);
-    tc_fence_after();
-    const int row = m0 + tid;  // warp w reads TMEM lanes 32w..32w+31
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
-    float* crow = nullptr;
-    if (row < v.M) {
-      if (KIND == GEMM_FPROP) crow = fprop_c_ptr(g, v, row, 0);
-      else if (KIND == GEMM_DGRAD) crow = dgrad_c_ptr(g, v, row, 0);
-      else crow = wgrad_c_ptr(g, v, row, 0);
-    }
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld16(taddr + c0, r);
-      tmem_ld_wait();
-      if (crow && n0 + c0 < v.N) {
+      // epilogue for row m0 + 32 q + lane
+      const int row = m0 + q * 32 + lane;
+      if (row < v.M) {
+        float* crow;
+        if (KIND == GEMM_FPROP) crow = fprop_c_ptr(g, v, row, 0);
+        else if (KIND == GEMM_DGRAD) crow = dgrad_c_ptr(g, v, row, 0);
+        else crow = wgrad_c_ptr(g, v, row, 0);
 #pragma unroll
-        for (int q = 0; q < 16; q += 4) {
-          const int n = n0 + c0 + q;
-          if (n >= v.N) break;
-          float o[4];
+        for (int c4 = 0; c4 < BN; c4 += 4) {
+          const int n = n0 + c4;
+          if (n < v.N) {
+            float o[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float x = __uint_as_float(r[q + u]);
-            const int nn = n + u;
-            if (KIND == GEMM_WGRAD) {
-              // handled below with accumulate
-            } else if (nn % a.c_pad < a.c_valid) {
-              if (v.bias) x += v.bias[nn];
-              x = act_fwd(a.act, x, a.slope);
-            } else {
-              x = 0.f;
+            for (int u = 0; u < 4; ++u) {
+              float x = acc[c4 + u];
+              if (KIND != GEMM_WGRAD) {
+                const int nn = n + u;
+                if (nn % a.c_pad < a.c_valid) {
+                  if (v.bias) x += v.bias[nn];
+                  x = act_fwd(a.act, x, a.slope);
+                } else {
+                  x = 0.f;
+                }
+              }
+              o[u] = x;
             }
-            o[u] = x;
+            float4* dst = reinterpret_cast<float4*>(crow + n);
+            if (KIND == GEMM_WGRAD && a.accumulate) {
+              const float4 old = *dst;
+              o[0] += old.x;
+              o[1] += old.y;
+              o[2] += old.z;
+              o[3] += old.w;
+            }
+            *dst = make_float4(o[0], o[1], o[2], o[3]);
           }
-          float4* dst = reinterpret_cast<float4*>(crow + n);
-          if (KIND == GEMM_WGRAD && a.accumulate) {
-            float4 old = *dst;
-            o[0] += old.x; o[1] += old.y; o[2] += old.z; o[3] += old.w;
-          }
-          *dst = make_float4(o[0], o[1], o[2], o[3]);
         }
       }
     }
@@ -401,18 +462,30 @@ __global__ void __launch_bounds__(NPROD + 32, 1) gemm_tc_kernel(GemmArgs a) {
   }
 }
 
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+  }
+  return n;
+}
+
 template <int KIND, int BN, int MODE>
 cudaError_t launch_bn(const GemmArgs& a, cudaStream_t st) {
-  constexpr int smem = smem_total(KIND, BN, MODE == MATH_TF32X3) + 1024;
+  constexpr int smem = smem_bytes(BN, MODE == MATH_TF32X3);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<KIND, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_tc_kernel<KIND, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((gemm_n(a) + BN - 1) / BN, (gemm_max_m(a) + BM - 1) / BM, a.L * gemm_phases(a));
-  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return cudaSuccess;
-  gemm_tc_kernel<KIND, BN, MODE><<<grid, NPROD + 32, smem, st>>>(a);
+  TileGrid tg{(gemm_n(a) + BN - 1) / BN, (gemm_max_m(a) + BM - 1) / BM, a.L * gemm_phases(a)};
+  if (tg.total() == 0) return cudaSuccess;
+  const int grid = std::min(tg.total(), sm_count());
+  gemm_tc_kernel<KIND, BN, MODE><<<grid, NTHREADS, smem, st>>>(a, tg);
   return launched();
 }
 
