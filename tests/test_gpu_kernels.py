@@ -43,6 +43,7 @@ CONV_CASES = [
     (3, 5, 7, 7, 6, 3, 2, 1),
     (2, 4, 6, 5, 4, 3, 1, 1),
     (2, 64, 8, 8, 128, 4, 2, 1),
+    (2, 64, 16, 16, 256, 4, 2, 1),
 ]
 
 
@@ -101,6 +102,7 @@ CONVT_CASES = [
     (3, 4, 3, 4, 6, 3, 2, 1),
     (2, 6, 5, 5, 4, 3, 1, 1),
     (2, 128, 7, 7, 64, 4, 2, 1),
+    (2, 256, 4, 4, 128, 4, 2, 1),
 ]
 
 
@@ -146,6 +148,42 @@ def test_convT2d_fwd_bwd(native, oracle, torch_cuda, case, math, tol):
         assert rel_max(nhwc_to_nchw(y[l], Cout), ry) < tol
         assert rel_max(nhwc_to_nchw(gx[l], Cin), rgx) < tol
         assert rel_max(convT_w_from_dev(gw[l], Cin, Cout, k), rgp[:nw].reshape(Cin, Cout, k, k)) < tol
+
+
+@pytest.mark.parametrize("dims", [(3, 64, 100, 6272), (2, 40, 6272, 4), (2, 300, 260, 200)])
+@pytest.mark.parametrize("math,tol", MODES)
+def test_dense_all_forms_multi_tile(native, torch_cuda, dims, math, tol):
+    """Dense fwd / bwd-data / bwd-filter with several M and N tiles (e.g. the
+    c1 generator head 100 -> 6272 and the discriminator head 6272 -> 1) vs an
+    f64 numpy reference."""
+    from paper_2102_10485_b200 import _native as N
+    torch = torch_cuda
+    L, B, nin, nout = dims
+    rng = np.random.default_rng(nin + nout)
+    x = rng.normal(size=(L, B, nin))
+    w = rng.normal(size=(L, nout, nin)) * 0.05
+    b = rng.normal(size=(L, nout))
+    gy = rng.normal(size=(L, B, nout))
+    pi, po = pad4(nin), pad4(nout)
+    xd = np.zeros((L, B, pi), np.float32); xd[..., :nin] = x
+    wd = np.zeros((L, po, pi), np.float32); wd[:, :nout, :nin] = w
+    bd = np.zeros((L, po), np.float32); bd[:, :nout] = b
+    gyd = np.zeros((L, B, po), np.float32); gyd[..., :nout] = gy
+    x_d, w_d, b_d, gy_d = dev(torch, xd), dev(torch, wd), dev(torch, bd), dev(torch, gyd)
+    y_d = torch.zeros((L, B, po), device="cuda")
+    gx_d = torch.zeros((L, B, pi), device="cuda")
+    gw_d = torch.zeros((L, po * pi), device="cuda")
+    N.check(native.pg_dense_fwd(L, B, nin, nout, ptr(x_d), ptr(w_d), po * pi, ptr(b_d), po, 0, 0.0, ptr(y_d), math,
+                                None), "fwd")
+    N.check(native.pg_dense_bwd_data(L, B, nin, nout, ptr(gy_d), ptr(w_d), po * pi, ptr(gx_d), math, None), "dgrad")
+    N.check(native.pg_dense_bwd_filter(L, B, nin, nout, ptr(x_d), ptr(gy_d), ptr(gw_d), po * pi, 0, math, None),
+            "wgrad")
+    y, gx, gw = host(y_d), host(gx_d), host(gw_d).reshape(L, po, pi)
+    xf, wf, gyf = xd.astype(np.float64)[..., :nin], wd.astype(np.float64)[:, :nout, :nin], gyd.astype(np.float64)[..., :nout]
+    for l in range(L):
+        assert rel_max(y[l][:, :nout], xf[l] @ wf[l].T + bd[l, :nout]) < tol
+        assert rel_max(gx[l][:, :nin], gyf[l] @ wf[l]) < tol
+        assert rel_max(gw[l][:nout, :nin], gyf[l].T @ xf[l]) < tol
 
 
 @pytest.mark.parametrize("math,tol", MODES)
