@@ -44,6 +44,9 @@ long long pg_launch_count(void);
  * record; read returns the summed device time of GEMM launches since enable */
 int pg_kernel_timing(int on);
 int pg_kernel_timing_read(double* gemm_ms);
+/* text report, one line per timed GEMM launch ("kind L= M= N= K= ... ms");
+ * returns the full length (copies at most cap-1 bytes + NUL) */
+long pg_kernel_timing_report(char* out, long cap);
 
 /* Convolution geometry of one layer for one label: input map H x W x Cin,
  * output map OH x OW x Cout, square kernel k, stride s, padding p, batch B.

@@ -109,6 +109,16 @@ int pg_kernel_timing_read(double* ms) {
   return guard([&] { *ms = pg::gemm_timing_read_ms(); });
 }
 
+long pg_kernel_timing_report(char* out, long cap) {
+  std::string r = pg::gemm_timing_report();
+  if (out && cap > 0) {
+    long n = std::min<long>(cap - 1, static_cast<long>(r.size()));
+    std::memcpy(out, r.data(), static_cast<size_t>(n));
+    out[n] = 0;
+  }
+  return static_cast<long>(r.size());
+}
+
 // ---------------- Conv2d ----------------
 int pg_conv2d_fwd(const pg_conv_desc* d, int L, const float* x, const float* w, long long w_ls, const float* bias,
                   long long bias_ls, int act, float slope, float* y, int math, void* stream) {

@@ -1,6 +1,8 @@
 // Engine selection for the implicit GEMMs, launch accounting and the
 // optional per-GEMM event timing used by bench.py's roofline figure.
 #include <atomic>
+#include <cstdio>
+#include <string>
 #include <mutex>
 #include <vector>
 
@@ -13,7 +15,22 @@ std::atomic<long long> g_launches{0};
 std::atomic<bool> g_timing{false};
 std::mutex g_mu;
 std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
+std::vector<std::string> g_tags;
 }  // namespace
+
+std::string gemm_timing_report() {
+  std::lock_guard<std::mutex> g(g_mu);
+  std::string out;
+  char buf[64];
+  for (size_t i = 0; i < g_events.size(); ++i) {
+    cudaEventSynchronize(g_events[i].second);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, g_events[i].first, g_events[i].second);
+    std::snprintf(buf, sizeof(buf), " %.4f\n", ms);
+    out += g_tags[i] + buf;
+  }
+  return out;
+}
 
 cudaError_t launched() {
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -29,6 +46,7 @@ void gemm_timing_enable(bool on) {
     cudaEventDestroy(e.second);
   }
   g_events.clear();
+  g_tags.clear();
   g_timing = on;
 }
 
@@ -55,8 +73,16 @@ cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
                                                                     : launch_gemm_simt(a, st);
   if (g_timing) {
     cudaEventRecord(e1, st);
+    char tag[160];
+    std::snprintf(tag, sizeof(tag), "%s L=%d M=%d N=%d K=%d phases=%d CS=%d CG=%d S=%dx%d G=%dx%d k=%d",
+                  a.kind == GEMM_FPROP ? "fprop" : a.kind == GEMM_DGRAD ? "dgrad" : "wgrad", a.L, gemm_max_m(a),
+                  gemm_n(a),
+                  a.kind == GEMM_FPROP ? a.g.k * a.g.k * a.g.CG
+                                       : a.kind == GEMM_WGRAD ? a.g.B * a.g.SH * a.g.SW : a.g.k * a.g.k * a.g.CS / (a.g.s * a.g.s),
+                  a.kind == GEMM_DGRAD ? a.g.s * a.g.s : 1, a.g.CS, a.g.CG, a.g.SH, a.g.SW, a.g.GH, a.g.GW, a.g.k);
     std::lock_guard<std::mutex> g(g_mu);
     g_events.emplace_back(e0, e1);
+    g_tags.emplace_back(tag);
   }
   return r;
 }

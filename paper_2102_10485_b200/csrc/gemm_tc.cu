@@ -4,10 +4,12 @@
 //
 // Persistent, warp-specialized; each CTA walks 128 x BN output tiles of the
 // (label, phase) problems in a static round-robin:
-//   warps 0-3  producers: gather the A / B tiles straight from the NHWC maps
-//              (implicit-GEMM index maps of gemm_gather.cuh with the per-row
-//              state hoisted out of the K loop), split hi/lo, write the UMMA
-//              canonical layouts, arrive on full[stage].
+//   warps 0-3  producers: cp.async-gather the A / B tiles straight from the
+//              NHWC maps into the UMMA canonical layouts (implicit-GEMM index
+//              maps of gemm_gather.cuh, per-row state hoisted out of the K
+//              loop, zero-fill for padding), STAGES-2 k-blocks in flight; in
+//              TF32X3 write lo = x - trunc_tf32(x) beside the raw tile (the
+//              raw fp32 tile is the hi operand: tcgen05 truncates to tf32).
 //   warp 4     the single MMA-issuing thread (and TMEM allocation): K is cut
 //              into segments of KSEG k-blocks; each segment accumulates into
 //              one of two TMEM buffers (ping-pong) and is committed to
@@ -29,6 +31,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm_gather.cuh"
 #include "kernels.hpp"
@@ -38,11 +41,12 @@ namespace pg {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 32;          // fp32 elements of K per stage
+constexpr int BK = 16;          // fp32 elements of K per stage
 constexpr int NPROD = 128;      // warps 0-3
 constexpr int NDRAIN = 128;     // warps 5-8
 constexpr int NTHREADS = NPROD + 32 + NDRAIN;
-constexpr int KSEG = 2;         // k-blocks per TMEM accumulation segment
+constexpr int KSEG = 4;         // k-blocks per TMEM accumulation segment (chain <= 24 MMA adds)
+__constant__ int c_dbg = 0;     // PG_TC_DEBUG bits: 1 no loads, 2 no split, 4 no MMA, 8 no drain loads
 
 // MN-major atom: 32 MN elements (128 B) x 4 K rows (128 B apart); the 16-byte
 // chunk bits [5,7) are XORed with the row bits [7,9).  Atoms MN-adjacent at
@@ -125,8 +129,12 @@ __host__ __device__ constexpr int stage_bytes(int bn, bool split) {
   return (tile_bytes(BM) + tile_bytes(bn)) * (split ? 2 : 1);
 }
 __host__ __device__ constexpr int num_stages(int bn, bool split) {
-  return stage_bytes(bn, split) * 4 <= 192 * 1024 ? 4 : (stage_bytes(bn, split) * 3 <= 192 * 1024 ? 3 : 2);
+  return 192 * 1024 / stage_bytes(bn, split) > 8 ? 8 : 192 * 1024 / stage_bytes(bn, split);
 }
+// k-blocks the producers run ahead; a stage is re-filled only after the MMA
+// released it two k-blocks earlier, so producers never wait on the MMA that
+// is currently running
+__host__ __device__ constexpr int lookahead(int stages) { return stages - 2 < 1 ? 1 : stages - 2; }
 __host__ __device__ constexpr int smem_bytes(int bn, bool split) {
   return num_stages(bn, split) * stage_bytes(bn, split) + 1024 /* barriers */ + 1024 /* alignment */;
 }
@@ -134,20 +142,22 @@ __host__ __device__ constexpr uint32_t tmem_cols(int bn) { return 2 * bn <= 32 ?
 
 PG_DEV float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-// store one float4 (hi, and lo when split) into a tile at byte offset off
-template <bool SPLIT>
-PG_DEV void put4(uint8_t* hi_tile, uint8_t* lo_tile, int off, float4 v) {
-  if (SPLIT) {
-    float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-    float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-    *reinterpret_cast<float4*>(hi_tile + off) = h;
-    *reinterpret_cast<float4*>(lo_tile + off) = l;
-  } else {
-    *reinterpret_cast<float4*>(hi_tile + off) = v;
-  }
-}
-
 PG_DEV float4 ld4(const float* p) { return p ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0, 0, 0, 0); }
+
+PG_DEV void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+PG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+PG_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// lo = x - trunc_tf32(x) for one 16-byte chunk (the raw chunk stays as "hi")
+PG_DEV void split4(const uint8_t* hi_tile, uint8_t* lo_tile, int off) {
+  const float4 v = *reinterpret_cast<const float4*>(hi_tile + off);
+  *reinterpret_cast<float4*>(lo_tile + off) =
+      make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z), v.w - tf32_hi(v.w));
+}
 
 // ---- per-row producer state for the K-major A operand (FPROP / DGRAD) ----
 struct RowState {
@@ -254,85 +264,163 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(GemmArgs a, TileGr
 
   if (warp < 4) {
     // ===================== producers =====================
+    // cp.async straight into the canonical layouts (zero-fill for padding),
+    // lookahead(STAGES) k-blocks in flight per thread; the raw fp32 tile is the "hi"
+    // operand as-is (the tensor core reads the top 19 bits of each fp32, i.e.
+    // truncates to tf32), and in TF32X3 each thread then writes lo = x -
+    // trunc_tf32(x) for exactly the chunks it copied.
     const int mn4 = tid % 32, krow0 = tid / 32;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const bool one_tap = (KIND == GEMM_FPROP ? g.CG : g.CS) % BK == 0;
+    // issue cursor: (tile, k-block) of the next k-block to fetch
+    int it_t = 0, it_kb = 0, it_nk = 0, im0 = 0, in0 = 0;
+    GemmView iv = make_view(a, 0, 0);
+    RowState irs = row_state<KIND>(g, iv, 0);
+    auto load_tile = [&](int t) -> bool {
       int z, mt, nt;
       tile_coords(tg, t, z, mt, nt);
-      const GemmView v = make_view(a, z / phases, z % phases);
-      const int m0 = mt * BM, n0 = nt * BN;
-      if (m0 >= v.M || n0 >= v.N) continue;
-      const int nk = (v.K + BK - 1) / BK;
-      const RowState rs = row_state<KIND>(g, v, m0 + tid);
-      const bool one_tap = (KIND == GEMM_FPROP ? g.CG : g.CS) % BK == 0;
-      for (int kb = 0; kb < nk; ++kb, ++kc) {
-        const int s = kc % STAGES;
-        mbar_wait(empty + s, ((kc / STAGES) & 1) ^ 1);
+      iv = make_view(a, z / phases, z % phases);
+      im0 = mt * BM;
+      in0 = nt * BN;
+      if (im0 >= iv.M || in0 >= iv.N) return false;
+      it_nk = (iv.K + BK - 1) / BK;
+      if (it_nk == 0) return false;
+      irs = row_state<KIND>(g, iv, im0 + tid);
+      return true;
+    };
+    auto seek = [&](int t) -> bool {
+      for (; t < ntiles; t += gridDim.x)
+        if (load_tile(t)) {
+          it_t = t;
+          it_kb = 0;
+          return true;
+        }
+      return false;
+    };
+    bool ivalid = seek(blockIdx.x);
+    uint32_t issued = 0, done = 0;
+
+    auto issue = [&]() {
+      const int s = issued % STAGES;
+      mbar_wait(empty + s, ((issued / STAGES) & 1) ^ 1);
+      const uint32_t a_hi = smem_u32(smem + s * STAGE);
+      const uint32_t b_hi = a_hi + A_BYTES;
+      const int k0 = it_kb * BK;
+      const GemmView& v = iv;
+      if (c_dbg & 1) goto issued_done;
+      // ---------------- A ----------------
+      if (!A_MN) {
+        // 128 rows x 8 chunks; this thread owns row tid
+        const uint32_t row_off = (tid / 8) * 128 + (tid % 8) * 16;
+        if (one_tap) {
+          const float* base = a_row_ptr<KIND>(g, v, irs, k0);
+#pragma unroll
+          for (int c = 0; c < BK / 4; ++c) {
+            const bool ok = base && k0 + 4 * c < v.K;
+            cp_async16(a_hi + c * (BM * 16) + row_off, ok ? base + 4 * c : v.A, ok);
+          }
+        } else {
+#pragma unroll 2
+          for (int c = 0; c < BK / 4; ++c) {
+            const float* p = a_row_ptr<KIND>(g, v, irs, k0 + 4 * c);
+            cp_async16(a_hi + c * (BM * 16) + row_off, p ? p : v.A, p != nullptr);
+          }
+        }
+      } else {
+        // WGRAD A[m = cs][k = spix] = smallg[spix][cs]: 32 float4 columns x 32 k rows
+#pragma unroll
+        for (int j = 0; j < BK / 4; ++j) {
+          const int kr = krow0 + 4 * j, k = k0 + kr, m = im0 + 4 * mn4;
+          const bool ok = k < v.K && m < v.M;
+          cp_async16(a_hi + mn_offset(BM, mn4, kr), ok ? v.A + (long long)k * g.CS + m : v.A, ok);
+        }
+      }
+      // ---------------- B ----------------
+      if (!B_MN) {
+        // FPROP: B[n][k] = W[n][k], rows contiguous over K; BN rows x 8 chunks
+#pragma unroll
+        for (int it = 0; it < (BN * (BK / 4) + NPROD - 1) / NPROD; ++it) {
+          const int item = tid + it * NPROD;
+          if (item < BN * (BK / 4)) {
+            const int c = item / BN, r = item % BN;
+            const int n = in0 + r, k = k0 + 4 * c;
+            const bool ok = n < v.N && k < v.K;
+            cp_async16(b_hi + c * (BN * 16) + (r / 8) * 128 + (r % 8) * 16, ok ? v.Bw + (long long)n * v.K + k : v.Bw,
+                       ok);
+          }
+        }
+      } else {
+        // MN-major B: (BN/4) float4 columns x 32 k rows
+        constexpr int COLS = BN / 4;
+        constexpr int ITEMS = COLS * BK;
+#pragma unroll
+        for (int it = 0; it < (ITEMS + NPROD - 1) / NPROD; ++it) {
+          const int item = tid + it * NPROD;
+          if (item < ITEMS) {
+            const int col = item % COLS, kr = item / COLS;
+            const int n = in0 + 4 * col, k = k0 + kr;
+            const float* p = nullptr;
+            if (n < v.N && k < v.K) {
+              if (KIND == GEMM_DGRAD) p = dgrad_b_ptr(g, v, n, k);
+              else p = wgrad_b_ptr(g, v, n, k);
+            }
+            cp_async16(b_hi + mn_offset(BN, col, kr), p ? p : v.Bw, p != nullptr);
+          }
+        }
+      }
+    issued_done:
+      ++issued;
+      if (++it_kb >= it_nk) ivalid = seek(it_t + gridDim.x);
+    };
+
+    auto finalize = [&]() {
+      const int s = done % STAGES;
+      if (SPLIT && !(c_dbg & 2)) {
         uint8_t* a_hi = smem + s * STAGE;
         uint8_t* b_hi = a_hi + A_BYTES;
         uint8_t* a_lo = b_hi + B_BYTES;
         uint8_t* b_lo = a_lo + A_BYTES;
-        const int k0 = kb * BK;
-        // ---------------- A ----------------
         if (!A_MN) {
-          // 128 rows x 8 chunks; this thread owns row tid
-          if (one_tap) {
-            const float* base = a_row_ptr<KIND>(g, v, rs, k0);
+          const int row_off = (tid / 8) * 128 + (tid % 8) * 16;
 #pragma unroll
-            for (int c = 0; c < BK / 4; ++c) {
-              const float* p = (base && k0 + 4 * c < v.K) ? base + 4 * c : nullptr;
-              put4<SPLIT>(a_hi, a_lo, c * (BM * 16) + (tid / 8) * 128 + (tid % 8) * 16, ld4(p));
-            }
-          } else {
-#pragma unroll 2
-            for (int c = 0; c < BK / 4; ++c) {
-              const float* p = a_row_ptr<KIND>(g, v, rs, k0 + 4 * c);
-              put4<SPLIT>(a_hi, a_lo, c * (BM * 16) + (tid / 8) * 128 + (tid % 8) * 16, ld4(p));
-            }
-          }
+          for (int c = 0; c < BK / 4; ++c) split4(a_hi, a_lo, c * (BM * 16) + row_off);
         } else {
-          // WGRAD A[m = cs][k = spix] = smallg[spix][cs]: 32 float4 columns x 32 k rows
 #pragma unroll
-          for (int j = 0; j < BK / 4; ++j) {
-            const int kr = krow0 + 4 * j, k = k0 + kr, m = m0 + 4 * mn4;
-            const float* p = (k < v.K && m < v.M) ? v.A + (long long)k * g.CS + m : nullptr;
-            put4<SPLIT>(a_hi, a_lo, mn_offset(BM, mn4, kr), ld4(p));
-          }
+          for (int j = 0; j < BK / 4; ++j) split4(a_hi, a_lo, mn_offset(BM, mn4, krow0 + 4 * j));
         }
-        // ---------------- B ----------------
         if (!B_MN) {
-          // FPROP: B[n][k] = W[n][k], rows contiguous over K; BN rows x 8 chunks
 #pragma unroll
           for (int it = 0; it < (BN * (BK / 4) + NPROD - 1) / NPROD; ++it) {
             const int item = tid + it * NPROD;
             if (item < BN * (BK / 4)) {
               const int c = item / BN, r = item % BN;
-              const int n = n0 + r, k = k0 + 4 * c;
-              const float* p = (n < v.N && k < v.K) ? v.Bw + (long long)n * v.K + k : nullptr;
-              put4<SPLIT>(b_hi, b_lo, c * (BN * 16) + (r / 8) * 128 + (r % 8) * 16, ld4(p));
+              split4(b_hi, b_lo, c * (BN * 16) + (r / 8) * 128 + (r % 8) * 16);
             }
           }
         } else {
-          // MN-major B: (BN/4) float4 columns x 32 k rows
           constexpr int COLS = BN / 4;
           constexpr int ITEMS = COLS * BK;
 #pragma unroll
           for (int it = 0; it < (ITEMS + NPROD - 1) / NPROD; ++it) {
             const int item = tid + it * NPROD;
-            if (item < ITEMS) {
-              const int col = item % COLS, kr = item / COLS;
-              const int n = n0 + 4 * col, k = k0 + kr;
-              const float* p = nullptr;
-              if (n < v.N && k < v.K) {
-                if (KIND == GEMM_DGRAD) p = dgrad_b_ptr(g, v, n, k);
-                else p = wgrad_b_ptr(g, v, n, k);
-              }
-              put4<SPLIT>(b_hi, b_lo, mn_offset(BN, col, kr), ld4(p));
-            }
+            if (item < ITEMS) split4(b_hi, b_lo, mn_offset(BN, item % COLS, item / COLS));
           }
         }
-        fence_async_smem();
-        mbar_arrive(full + s);
       }
+      fence_async_smem();
+      mbar_arrive(full + s);
+      ++done;
+    };
+
+    constexpr int D = lookahead(STAGES);
+    for (int d = 0; d < D; ++d) {
+      if (ivalid) issue();
+      cp_async_commit();
+    }
+    while (done < issued) {
+      if (ivalid) issue();
+      cp_async_commit();
+      cp_async_wait<D>();
+      finalize();
     }
   } else if (warp == 4) {
     // ===================== MMA issuer =====================
@@ -368,7 +456,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(GemmArgs a, TileGr
               const uint64_t ah = make_desc(a_hi + kk * astep, alb, asb, alay);
               const uint64_t bh = make_desc(b_hi + kk * bstep, blb, bsb, blay);
               const uint32_t acc = (kb != k_seg || kk) ? 1u : 0u;
-              if (SPLIT) {
+              if (c_dbg & 4) {
+              } else if (SPLIT) {
                 const uint64_t al = make_desc(a_lo + kk * astep, alb, asb, alay);
                 const uint64_t bl = make_desc(b_lo + kk * bstep, blb, bsb, blay);
                 mma_tf32(d, al, bh, idesc, acc);  // small terms first
@@ -406,6 +495,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(GemmArgs a, TileGr
 #pragma unroll
         for (int c = 0; c < BN / 16; ++c) {
           uint32_t r[16];
+          if (c_dbg & 8) continue;
           tmem_ld16(tmem + lane_base + buf * BN + c * 16, r);
           tmem_ld_wait();
 #pragma unroll
@@ -517,6 +607,13 @@ bool gemm_tc_supported(const GemmArgs& a) {
 }
 
 cudaError_t launch_gemm_tc(const GemmArgs& a, int math, cudaStream_t st) {
+  static bool dbg_set = false;
+  if (!dbg_set) {
+    const char* e = std::getenv("PG_TC_DEBUG");
+    int v = e ? std::atoi(e) : 0;
+    cudaMemcpyToSymbol(c_dbg, &v, sizeof(int));
+    dbg_set = true;
+  }
   if (math == MATH_TF32) return launch_mode<MATH_TF32>(a, st);
   return launch_mode<MATH_TF32X3>(a, st);
 }

@@ -15,6 +15,10 @@ long long launch_count();
 // optional per-GEMM timing (CUDA events on the launching stream)
 void gemm_timing_enable(bool on);
 double gemm_timing_read_ms();
+}  // namespace pg
+#include <string>
+namespace pg {
+std::string gemm_timing_report();  // one line per timed GEMM launch: shape tags + ms
 
 int gemm_max_m(const GemmArgs& a);
 int gemm_n(const GemmArgs& a);
