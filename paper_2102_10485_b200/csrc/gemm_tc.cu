@@ -153,9 +153,8 @@ PG_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 // lo = x - trunc_tf32(x) for one 16-byte chunk (the raw chunk stays as "hi")
-PG_DEV void split4(const uint8_t* hi_tile, uint8_t* lo_tile, int off) {
-  const float4 v = *reinterpret_cast<const float4*>(hi_tile + off);
-  *reinterpret_cast<float4*>(lo_tile + off) =
+PG_DEV void store_lo(uint8_t* dst, float4 v) {
+  *reinterpret_cast<float4*>(dst) =
       make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z), v.w - tf32_hi(v.w));
 }
 
@@ -372,6 +371,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(GemmArgs a, TileGr
       if (++it_kb >= it_nk) ivalid = seek(it_t + gridDim.x);
     };
 
+    // chunk offsets this thread owns in every stage (identical for issue and split)
+    constexpr int NA = BK / 4;
+    constexpr int NB_ITEMS = BN * (BK / 4);  // same count for both B layouts
+    constexpr int NB = (NB_ITEMS + NPROD - 1) / NPROD;
+    int a_off[NA], b_off[NB];
+#pragma unroll
+    for (int c = 0; c < NA; ++c)
+      a_off[c] = A_MN ? mn_offset(BM, mn4, krow0 + 4 * c) : c * (BM * 16) + (tid / 8) * 128 + (tid % 8) * 16;
+#pragma unroll
+    for (int it = 0; it < NB; ++it) {
+      const int item = tid + it * NPROD;
+      if (B_MN) b_off[it] = mn_offset(BN, item % (BN / 4), item / (BN / 4));
+      else b_off[it] = (item / BN) * (BN * 16) + ((item % BN) / 8) * 128 + (item % 8) * 16;
+      if (item >= NB_ITEMS) b_off[it] = -1;
+    }
+
     auto finalize = [&]() {
       const int s = done % STAGES;
       if (SPLIT && !(c_dbg & 2)) {
@@ -379,32 +394,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(GemmArgs a, TileGr
         uint8_t* b_hi = a_hi + A_BYTES;
         uint8_t* a_lo = b_hi + B_BYTES;
         uint8_t* b_lo = a_lo + A_BYTES;
-        if (!A_MN) {
-          const int row_off = (tid / 8) * 128 + (tid % 8) * 16;
+        // all loads first (independent), then the splits and stores
+        float4 va[NA], vb[NB];
 #pragma unroll
-          for (int c = 0; c < BK / 4; ++c) split4(a_hi, a_lo, c * (BM * 16) + row_off);
-        } else {
+        for (int c = 0; c < NA; ++c) va[c] = *reinterpret_cast<const float4*>(a_hi + a_off[c]);
 #pragma unroll
-          for (int j = 0; j < BK / 4; ++j) split4(a_hi, a_lo, mn_offset(BM, mn4, krow0 + 4 * j));
-        }
-        if (!B_MN) {
+        for (int it = 0; it < NB; ++it)
+          if (b_off[it] >= 0) vb[it] = *reinterpret_cast<const float4*>(b_hi + b_off[it]);
 #pragma unroll
-          for (int it = 0; it < (BN * (BK / 4) + NPROD - 1) / NPROD; ++it) {
-            const int item = tid + it * NPROD;
-            if (item < BN * (BK / 4)) {
-              const int c = item / BN, r = item % BN;
-              split4(b_hi, b_lo, c * (BN * 16) + (r / 8) * 128 + (r % 8) * 16);
-            }
-          }
-        } else {
-          constexpr int COLS = BN / 4;
-          constexpr int ITEMS = COLS * BK;
+        for (int c = 0; c < NA; ++c) store_lo(a_lo + a_off[c], va[c]);
 #pragma unroll
-          for (int it = 0; it < (ITEMS + NPROD - 1) / NPROD; ++it) {
-            const int item = tid + it * NPROD;
-            if (item < ITEMS) split4(b_hi, b_lo, mn_offset(BN, item % COLS, item / COLS));
-          }
-        }
+        for (int it = 0; it < NB; ++it)
+          if (b_off[it] >= 0) store_lo(b_lo + b_off[it], vb[it]);
       }
       fence_async_smem();
       mbar_arrive(full + s);
