@@ -32,6 +32,26 @@ std::string gemm_timing_report() {
   return out;
 }
 
+// grow-only device scratch shared by the split-K paths (stream-ordered users)
+float* gemm_scratch(size_t floats, cudaStream_t st) {
+  static float* buf = nullptr;
+  static size_t cap = 0;
+  std::lock_guard<std::mutex> g(g_mu);
+  if (floats > cap) {
+    if (buf) {
+      cudaStreamSynchronize(st);
+      cudaFree(buf);
+    }
+    buf = nullptr;
+    if (cudaMalloc(&buf, floats * sizeof(float)) != cudaSuccess) {
+      cap = 0;
+      return nullptr;
+    }
+    cap = floats;
+  }
+  return buf;
+}
+
 cudaError_t launched() {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();

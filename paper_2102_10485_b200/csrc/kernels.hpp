@@ -27,6 +27,7 @@ cudaError_t launch_gemm_tc(const GemmArgs& a, int math, cudaStream_t st);  // tc
 bool gemm_tc_supported(const GemmArgs& a);
 cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st);  // thin.cu
 bool gemm_thin_supported(const GemmArgs& a);
+float* gemm_scratch(size_t floats, cudaStream_t st);  // grow-only workspace for split-K reductions
 // picks the engine for a math mode and problem shape
 cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st);
 

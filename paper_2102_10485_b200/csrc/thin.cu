@@ -8,9 +8,8 @@
 //   thin_in_fprop   FPROP with CG == 4, CS <= 64 (discriminator first conv,
 //                   generator output ConvT bwd-data): one thread per output
 //                   pixel, all CS channels in registers, weights in smem
-//   thin_in_wgrad   WGRAD with CG == 4, CS <= 64: one block per label,
-//                   one thread per (cs, tap) accumulating its 4 channels over
-//                   every small-map pixel in a fixed order (deterministic)
+//   thin_in_wgrad   WGRAD with CG == 4, CS <= 64, k*k <= 16: split-K SIMT
+//                   GEMM over fixed pixel chunks + fixed-order chunk reduce
 //   dense_*         the dense heads: FPROP with N <= 4 (warp dot products),
 //                   FPROP with small K (weights streamed once), DGRAD with
 //                   K <= 4 and WGRAD with M <= 4 (outer products)
@@ -115,53 +114,76 @@ __global__ void __launch_bounds__(128) thin_in_fprop_kernel(GemmArgs a) {
 
 // ---- WGRAD, CG == 4, CS <= 64 ---------------------------------------------
 // dW[cs][tap][0:4] (+)= sum_{spix} smallg[spix][cs] * big[gather(spix, tap)][0:4]
-constexpr int TW_CHUNK = 32;  // small-map pixels staged per iteration
-__global__ void __launch_bounds__(1024) thin_in_wgrad_kernel(GemmArgs a) {
+// A small GEMM (M = CS, N = k*k*4, K = small-map pixels) split over K into
+// fixed chunks: block (chunk, label) computes the whole CS x N partial with a
+// register-tiled SIMT loop over 32-pixel smem stages; a second kernel sums the
+// chunk partials in chunk order (deterministic, no atomics).
+constexpr int TW_KC = 32;      // pixels per smem stage
+constexpr int TW_SPLIT = 1024; // pixels per chunk
+__global__ void __launch_bounds__(256) thin_in_wgrad_partial_kernel(GemmArgs a, float* part, int nchunk) {
   const ConvGeo& g = a.g;
-  const int l = blockIdx.x;
-  const int kk = g.k * g.k;
-  const int pairs = g.CS * kk;
+  const int l = blockIdx.y, chunk = blockIdx.x;
+  const int kk = g.k * g.k, NN = kk * 4;  // N <= 64
   const float* sg = a.small + l * a.small_ls;
   const float* big = a.big + l * a.big_ls;
-  __shared__ float gs[TW_CHUNK][64];
+  __shared__ float gs[TW_KC][64];
+  __shared__ float xs[TW_KC][64];
   const int tid = threadIdx.x;
-  const int cs = tid / kk, tap = tid % kk;
-  const bool active = tid < pairs;
-  const int ki = tap / g.k, kj = tap % g.k;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int tm = tid / 16, tn = tid % 16;  // 4x4 micro tile at (4 tm, 4 tn)
+  float acc[4][4] = {};
   const long long K = (long long)g.B * g.SH * g.SW;
-  for (long long k0 = 0; k0 < K; k0 += TW_CHUNK) {
+  const long long k_begin = (long long)chunk * TW_SPLIT;
+  const long long k_end = k_begin + TW_SPLIT < K ? k_begin + TW_SPLIT : K;
+  for (long long k0 = k_begin; k0 < k_end; k0 += TW_KC) {
     __syncthreads();
-    for (int e = tid; e < TW_CHUNK * g.CS; e += blockDim.x) {
-      const long long sp = k0 + e / g.CS;
-      gs[e / g.CS][e % g.CS] = sp < K ? sg[sp * g.CS + e % g.CS] : 0.f;
-    }
-    __syncthreads();
-    if (!active) continue;
-    for (int q = 0; q < TW_CHUNK; ++q) {
+    for (int e = tid; e < TW_KC * 64; e += 256) {
+      const int q = e / 64, c = e % 64;
       const long long sp = k0 + q;
-      if (sp >= K) break;
-      const int j = (int)(sp % g.SW);
-      const long long t = sp / g.SW;
-      const int i = (int)(t % g.SH), b = (int)(t / g.SH);
-      const int y = i * g.s - g.p + ki, x = j * g.s - g.p + kj;
-      if (y < 0 || y >= g.GH || x < 0 || x >= g.GW) continue;
-      const float4 v = __ldg(reinterpret_cast<const float4*>(big + (((long long)b * g.GH + y) * g.GW + x) * 4));
-      const float gv = gs[q][cs];
-      acc[0] = fmaf(gv, v.x, acc[0]);
-      acc[1] = fmaf(gv, v.y, acc[1]);
-      acc[2] = fmaf(gv, v.z, acc[2]);
-      acc[3] = fmaf(gv, v.w, acc[3]);
+      float gv = 0.f, xv = 0.f;
+      if (sp < k_end) {
+        if (c < g.CS) gv = sg[sp * g.CS + c];
+        if (c < NN) {
+          const int tap = c / 4, cg = c % 4;
+          const int j = (int)(sp % g.SW);
+          const long long t = sp / g.SW;
+          const int i = (int)(t % g.SH), b = (int)(t / g.SH);
+          const int y = i * g.s - g.p + tap / g.k, x = j * g.s - g.p + tap % g.k;
+          if (y >= 0 && y < g.GH && x >= 0 && x < g.GW) xv = big[(((long long)b * g.GH + y) * g.GW + x) * 4 + cg];
+        }
+      }
+      gs[q][c] = gv;
+      xs[q][c] = xv;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int q = 0; q < TW_KC; ++q) {
+      const float4 av = *reinterpret_cast<const float4*>(&gs[q][tm * 4]);
+      const float4 bv = *reinterpret_cast<const float4*>(&xs[q][tn * 4]);
+      const float ar[4] = {av.x, av.y, av.z, av.w}, br[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ar[u], br[v], acc[u][v]);
     }
   }
-  if (!active) return;
-  float4* out = reinterpret_cast<float4*>(a.out + l * a.out_ls + (long long)(cs * kk + tap) * 4);
-  float4 r = make_float4(acc[0], acc[1], acc[2], acc[3]);
-  if (a.accumulate) {
-    const float4 o = *out;
-    r.x += o.x; r.y += o.y; r.z += o.z; r.w += o.w;
-  }
-  *out = r;
+  float* dst = part + ((long long)l * nchunk + chunk) * 64 * 64;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    *reinterpret_cast<float4*>(dst + (tm * 4 + u) * 64 + tn * 4) =
+        make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+}
+
+__global__ void thin_in_wgrad_reduce_kernel(GemmArgs a, const float* part, int nchunk) {
+  const ConvGeo& g = a.g;
+  const int l = blockIdx.y;
+  const int NN = g.k * g.k * 4;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // over CS x NN
+  if (e >= g.CS * NN) return;
+  const int m = e / NN, n = e % NN;
+  float s = 0.f;
+  for (int c = 0; c < nchunk; ++c) s += part[(((long long)l * nchunk + c) * 64 + m) * 64 + n];
+  float* out = a.out + l * a.out_ls + e;
+  *out = a.accumulate ? *out + s : s;
 }
 
 // ---- dense heads ----------------------------------------------------------
@@ -297,7 +319,7 @@ Thin classify(const GemmArgs& a) {
   }
   if (a.kind == GEMM_DGRAD && g.CG <= 4) return T_OUT_DGRAD;
   if (a.kind == GEMM_FPROP && g.CG == 4 && g.CS <= 64) return T_IN_FPROP;
-  if (a.kind == GEMM_WGRAD && g.CG == 4 && g.CS <= 64 && g.CS * g.k * g.k <= 1024) return T_IN_WGRAD;
+  if (a.kind == GEMM_WGRAD && g.CG == 4 && g.CS <= 64 && g.k * g.k <= 16) return T_IN_WGRAD;
   return T_NONE;
 }
 
@@ -322,9 +344,18 @@ cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st) {
       else thin_in_fprop_kernel<64><<<grid, 128, smem, st>>>(a);
       break;
     }
-    case T_IN_WGRAD:
-      thin_in_wgrad_kernel<<<a.L, 1024, 0, st>>>(a);
+    case T_IN_WGRAD: {
+      const long long K = (long long)g.B * g.SH * g.SW;
+      const int nchunk = (int)((K + TW_SPLIT - 1) / TW_SPLIT);
+      float* part = gemm_scratch((size_t)a.L * nchunk * 64 * 64, st);
+      if (!part) return cudaErrorMemoryAllocation;
+      thin_in_wgrad_partial_kernel<<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
+      cudaError_t e = launched();
+      if (e != cudaSuccess) return e;
+      const int nout = g.CS * g.k * g.k * 4;
+      thin_in_wgrad_reduce_kernel<<<dim3((nout + 255) / 256, a.L), 256, 0, st>>>(a, part, nchunk);
       break;
+    }
     case T_D_FPROP_N4:
       dense_fprop_n4_kernel<<<dim3((unsigned)((g.B * 32 + 255) / 256), a.L), 256, 0, st>>>(a);
       break;

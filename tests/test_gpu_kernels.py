@@ -44,6 +44,8 @@ CONV_CASES = [
     (2, 4, 6, 5, 4, 3, 1, 1),
     (2, 64, 8, 8, 128, 4, 2, 1),
     (2, 64, 16, 16, 256, 4, 2, 1),
+    (16, 3, 32, 32, 64, 4, 2, 1),
+    (4, 1, 28, 28, 64, 4, 2, 1),
 ]
 
 
@@ -103,6 +105,8 @@ CONVT_CASES = [
     (2, 6, 5, 5, 4, 3, 1, 1),
     (2, 128, 7, 7, 64, 4, 2, 1),
     (2, 256, 4, 4, 128, 4, 2, 1),
+    (16, 64, 16, 16, 3, 4, 2, 1),
+    (4, 64, 14, 14, 1, 4, 2, 1),
 ]
 
 
@@ -150,7 +154,8 @@ def test_convT2d_fwd_bwd(native, oracle, torch_cuda, case, math, tol):
         assert rel_max(convT_w_from_dev(gw[l], Cin, Cout, k), rgp[:nw].reshape(Cin, Cout, k, k)) < tol
 
 
-@pytest.mark.parametrize("dims", [(3, 64, 100, 6272), (2, 40, 6272, 4), (2, 300, 260, 200)])
+@pytest.mark.parametrize("dims", [(3, 64, 100, 6272), (2, 40, 6272, 4), (2, 300, 260, 200), (2, 16, 100, 4096),
+                                  (2, 16, 4096, 1), (2, 4, 8192, 1), (2, 4, 100, 8192)])
 @pytest.mark.parametrize("math,tol", MODES)
 def test_dense_all_forms_multi_tile(native, torch_cuda, dims, math, tol):
     """Dense fwd / bwd-data / bwd-filter with several M and N tiles (e.g. the
