@@ -13,7 +13,7 @@ import oracle_lib
 from paper_2102_10485_b200 import GroupSpec, LabelGroup, _native as N, baseline_arch
 from parity import layer_tensors
 
-cfg, L, per_label, B = 1, 2, 128, 64
+cfg, L, per_label, B = (int(x) for x in (sys.argv[1:5] if len(sys.argv) > 4 else (1, 2, 128, 64)))
 arch = baseline_arch(cfg)
 orc = oracle_lib.OracleGroup(64, cfg, L, per_label, B, data_seed=3, base_seed=7)
 orc.step(1)
@@ -23,8 +23,10 @@ for math in (0, 1):
     grp.generate_dataset(3)
     grp.train_steps(1)
     print(f"=== math {math}: reports", grp.reports(0)[-1], orc.get(0, 10)[-4:])
-    for net, gcode, spec, ish in (("D", N.F_DISC_GRADS, arch.disc, arch.image), ("G", N.F_GEN_GRADS, arch.gen, (100,))):
-        g, r = grp.get(0, gcode), orc.get(0, gcode)
+    for lab in range(L):
+     print(f"  -- label {lab}: reports", grp.reports(lab)[-1], orc.get(lab, 10)[-4:])
+     for net, gcode, spec, ish in (("D", N.F_DISC_GRADS, arch.disc, arch.image), ("G", N.F_GEN_GRADS, arch.gen, (100,))):
+        g, r = grp.get(lab, gcode), orc.get(lab, gcode)
         for name, off, n, fb in layer_tensors(spec, ish):
             a, b = g[off:off + n], r[off:off + n]
             e = np.abs(a - b)

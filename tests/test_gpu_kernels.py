@@ -46,6 +46,9 @@ CONV_CASES = [
     (2, 64, 16, 16, 256, 4, 2, 1),
     (16, 3, 32, 32, 64, 4, 2, 1),
     (4, 1, 28, 28, 64, 4, 2, 1),
+    (4, 256, 8, 8, 512, 4, 2, 1),
+    (4, 128, 16, 16, 256, 4, 2, 1),
+    (4, 64, 32, 32, 128, 4, 2, 1),
 ]
 
 
@@ -107,6 +110,9 @@ CONVT_CASES = [
     (2, 256, 4, 4, 128, 4, 2, 1),
     (16, 64, 16, 16, 3, 4, 2, 1),
     (4, 64, 14, 14, 1, 4, 2, 1),
+    (4, 512, 4, 4, 256, 4, 2, 1),
+    (4, 256, 8, 8, 128, 4, 2, 1),
+    (4, 128, 16, 16, 64, 4, 2, 1),
 ]
 
 
