@@ -49,6 +49,10 @@ CONV_CASES = [
     (4, 256, 8, 8, 512, 4, 2, 1),
     (4, 128, 16, 16, 256, 4, 2, 1),
     (4, 64, 32, 32, 128, 4, 2, 1),
+    # TMA engine edge cases: padded 7x7 output boxes, batch not a multiple of the box depth
+    (3, 64, 14, 14, 128, 4, 2, 1),
+    (5, 128, 8, 8, 256, 4, 2, 1),
+    (3, 32, 16, 16, 32, 4, 2, 1),
 ]
 
 
@@ -113,6 +117,8 @@ CONVT_CASES = [
     (4, 512, 4, 4, 256, 4, 2, 1),
     (4, 256, 8, 8, 128, 4, 2, 1),
     (4, 128, 16, 16, 64, 4, 2, 1),
+    (3, 256, 4, 4, 128, 4, 2, 1),
+    (3, 64, 7, 7, 32, 4, 2, 1),
 ]
 
 
