@@ -13,6 +13,8 @@
 //   dense_*         the dense heads: FPROP with N <= 4 (warp dot products),
 //                   FPROP with small K (weights streamed once), DGRAD with
 //                   K <= 4 and WGRAD with M <= 4 (outer products)
+#include <algorithm>
+
 #include "gemm_gather.cuh"
 #include "kernels.hpp"
 
@@ -26,136 +28,240 @@ PG_DEV float epi(const GemmArgs& a, const float* bias, int n, float x) {
   return act_fwd(a.act, x, a.slope);
 }
 
+PG_DEV int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
 // ---- DGRAD, N = CG <= 4 ---------------------------------------------------
 // out[b][y][x][0:4] = sum_{valid taps, cs} small[b][i][j][cs] * W[cs][ki][kj][0:4]
-__global__ void __launch_bounds__(256) thin_out_dgrad_kernel(GemmArgs a) {
+// Block = OD_TY x OD_TX output tile of one image.  The small-map patch every
+// tap of the tile reaches is staged in shared memory by coalesced float4
+// copies, with a padded pixel stride (CS + 4 floats) so the per-pixel float4
+// reads of a warp are bank-conflict free; the label's weights sit beside it
+// as one float4 per (cs, tap) (the <= 4 output channels).  Thread = two
+// same-phase output pixels (x, x + s) of a row: every weight float4 feeds 8 FMAs.
+constexpr int OD_TX = 64, OD_TY = 4, OD_THREADS = OD_TX / 2 * OD_TY;
+__host__ __device__ inline int od_patch(int t, int k, int s) { return (t + k - 2) / s + 2; }
+
+__global__ void __launch_bounds__(OD_THREADS) thin_out_dgrad_kernel(GemmArgs a) {
+  extern __shared__ float4 sm4[];
   const ConvGeo& g = a.g;
-  const int l = blockIdx.y;
-  const long long npix = (long long)g.B * g.GH * g.GW;
-  const long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (pix >= npix) return;
-  const float* small = a.small + l * a.small_ls;
+  const int kk = g.k * g.k;
+  const int PR = od_patch(OD_TY, g.k, g.s), PC = od_patch(OD_TX, g.k, g.s), PS = g.CS + 4;
+  float4* wsm4 = sm4;
+  float* patch = reinterpret_cast<float*>(sm4 + g.CS * kk);
+  const int ntx = (g.GW + OD_TX - 1) / OD_TX;
+  const int x_lo = (blockIdx.x % ntx) * OD_TX, y_lo = (blockIdx.x / ntx) * OD_TY;
+  const int b = blockIdx.y, l = blockIdx.z;
+  const int i_lo = floordiv(y_lo + g.p - g.k + 1, g.s), j_lo = floordiv(x_lo + g.p - g.k + 1, g.s);
   const float* w = a.w + l * a.w_ls;
-  const int x = (int)(pix % g.GW);
-  const long long t = pix / g.GW;
-  const int y = (int)(t % g.GH), b = (int)(t / g.GH);
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int e = threadIdx.x; e < g.CS * kk; e += blockDim.x) {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int n = 0; n < g.CG; ++n) v[n] = w[(long long)e * g.CG + n];
+    wsm4[e] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  const float* small = a.small + l * a.small_ls + (long long)b * g.SH * g.SW * g.CS;
+  const int c4n = g.CS / 4;
+  for (int e = threadIdx.x; e < PR * PC * c4n; e += blockDim.x) {
+    const int c4 = e % c4n, pix = e / c4n;
+    const int i = i_lo + pix / PC, j = j_lo + pix % PC;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i >= 0 && i < g.SH && j >= 0 && j < g.SW)
+      v = __ldg(reinterpret_cast<const float4*>(small + ((long long)i * g.SW + j) * g.CS) + c4);
+    *reinterpret_cast<float4*>(patch + pix * PS + 4 * c4) = v;
+  }
+  __syncthreads();
+  const int q = threadIdx.x % (OD_TX / 2);
+  const int y = y_lo + threadIdx.x / (OD_TX / 2);
+  const int x0 = x_lo + (q / g.s) * (2 * g.s) + q % g.s;
+  if (y >= g.GH) return;
+  float acc[2][4];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) acc[u][n] = 0.f;
   for (int ki = (y + g.p) % g.s; ki < g.k; ki += g.s) {
     const int i = (y + g.p - ki) / g.s;
     if (i < 0 || i >= g.SH) continue;
-    for (int kj = (x + g.p) % g.s; kj < g.k; kj += g.s) {
-      const int j = (x + g.p - kj) / g.s;
-      if (j < 0 || j >= g.SW) continue;
-      const float4* src = reinterpret_cast<const float4*>(small + (((long long)b * g.SH + i) * g.SW + j) * g.CS);
-      const float* wt = w + (ki * g.k + kj) * g.CG;
-      for (int c4 = 0; c4 < g.CS / 4; ++c4) {
-        const float4 v = __ldg(src + c4);
-        const float vv[4] = {v.x, v.y, v.z, v.w};
+    for (int kj = (x0 + g.p) % g.s; kj < g.k; kj += g.s) {
+      const int tap = ki * g.k + kj;
+      const float* src[2];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float* wr = wt + (long long)(c4 * 4 + u) * g.k * g.k * g.CG;
+      for (int u = 0; u < 2; ++u) {
+        const int x = x0 + g.s * u;
+        const int j = (x + g.p - kj) / g.s;
+        src[u] = (x < g.GW && j >= 0 && j < g.SW) ? patch + ((i - i_lo) * PC + (j - j_lo)) * PS : nullptr;
+      }
+      for (int c4 = 0; c4 < c4n; ++c4) {
+        float4 v[2];
 #pragma unroll
-          for (int n = 0; n < 4; ++n)
-            if (n < g.CG) acc[n] = fmaf(vv[u], __ldg(wr + n), acc[n]);
+        for (int u = 0; u < 2; ++u)
+          v[u] = src[u] ? *reinterpret_cast<const float4*>(src[u] + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const float4 wv = wsm4[(c4 * 4 + cc) * kk + tap];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float sv = cc == 0 ? v[u].x : cc == 1 ? v[u].y : cc == 2 ? v[u].z : v[u].w;
+            acc[u][0] = fmaf(sv, wv.x, acc[u][0]);
+            acc[u][1] = fmaf(sv, wv.y, acc[u][1]);
+            acc[u][2] = fmaf(sv, wv.z, acc[u][2]);
+            acc[u][3] = fmaf(sv, wv.w, acc[u][3]);
+          }
         }
       }
     }
   }
-  float* out = a.out + l * a.out_ls + pix * g.CG;
   const float* bias = a.bias ? a.bias + l * a.bias_ls : nullptr;
-  for (int n = 0; n < g.CG; ++n) out[n] = epi(a, bias, n, acc[n]);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int x = x0 + g.s * u;
+    if (x >= g.GW) continue;
+    float* o = a.out + l * a.out_ls + (((long long)b * g.GH + y) * g.GW + x) * g.CG;
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+      if (n < g.CG) o[n] = epi(a, bias, n, acc[u][n]);
+  }
 }
 
 // ---- FPROP, CG == 4, CS <= 64 ---------------------------------------------
 // out[b][i][j][cs] = sum_{tap} big[b][y][x][0:4] . W[cs][tap][0:4]
-template <int CSMAX>
-__global__ void __launch_bounds__(128) thin_in_fprop_kernel(GemmArgs a) {
-  extern __shared__ float wsm[];  // [CS][k*k][4]
+// Block = IF_PIX output pixels of one image (TI rows x TJ cols) x all CS
+// channels.  The input patch under the tile ((TI-1)s+k rows x (TJ-1)s+k
+// columns of 4-channel pixels) and the weights (one float4 per (cs, tap)) are
+// staged in shared memory.  Thread = two output pixels x 16 channels (the
+// channel group is warp-uniform, so weight reads are broadcasts): each weight
+// float4 feeds 8 FMAs, registers stay low enough for full occupancy.
+constexpr int IF_PIX = 128, IF_THREADS = 256, IF_CSG = 16;
+
+__global__ void __launch_bounds__(IF_THREADS) thin_in_fprop_kernel(GemmArgs a, int TI, int TJ) {
+  extern __shared__ float4 sm4[];
   const ConvGeo& g = a.g;
-  const int l = blockIdx.y;
   const int kk = g.k * g.k;
-  const float* w = a.w + l * a.w_ls;
-  for (int e = threadIdx.x; e < g.CS * kk * 4; e += blockDim.x) wsm[e] = w[e];
+  const int PR = (TI - 1) * g.s + g.k, PC = (TJ - 1) * g.s + g.k;
+  float4* wsm4 = sm4;               // [64][kk], zero beyond CS
+  float4* patch = sm4 + 64 * kk;    // [PR][PC]
+  const int ntj = (g.SW + TJ - 1) / TJ;
+  const int j0 = (blockIdx.x % ntj) * TJ, i0 = (blockIdx.x / ntj) * TI;
+  const int b = blockIdx.y, l = blockIdx.z;
+  const float4* w = reinterpret_cast<const float4*>(a.w + l * a.w_ls);
+  for (int e = threadIdx.x; e < 64 * kk; e += blockDim.x)
+    wsm4[e] = e < g.CS * kk ? w[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* big = a.big + l * a.big_ls + (long long)b * g.GH * g.GW * 4;
+  const int y_lo = i0 * g.s - g.p, x_lo = j0 * g.s - g.p;
+  for (int e = threadIdx.x; e < PR * PC; e += blockDim.x) {
+    const int y = y_lo + e / PC, x = x_lo + e % PC;
+    patch[e] = (y >= 0 && y < g.GH && x >= 0 && x < g.GW)
+                   ? __ldg(reinterpret_cast<const float4*>(big + ((long long)y * g.GW + x) * 4))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   __syncthreads();
-  const long long npix = (long long)g.B * g.SH * g.SW;
-  const long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (pix >= npix) return;
-  const float* big = a.big + l * a.big_ls;
-  const int j = (int)(pix % g.SW);
-  const long long t = pix / g.SW;
-  const int i = (int)(t % g.SH), b = (int)(t / g.SH);
-  float acc[CSMAX];
+  const int cs0 = (threadIdx.x / (IF_PIX / 2)) * IF_CSG;
+  if (cs0 >= g.CS) return;
+  const int pp = threadIdx.x % (IF_PIX / 2);
+  int ii[2], jj[2];
+  bool ok[2];
 #pragma unroll
-  for (int c = 0; c < CSMAX; ++c) acc[c] = 0.f;
+  for (int u = 0; u < 2; ++u) {
+    const int pix = pp + u * (IF_PIX / 2);
+    ii[u] = pix / TJ;
+    jj[u] = pix % TJ;
+    ok[u] = ii[u] < TI && i0 + ii[u] < g.SH && j0 + jj[u] < g.SW;
+  }
+  float acc[2][IF_CSG];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int c = 0; c < IF_CSG; ++c) acc[u][c] = 0.f;
   for (int ki = 0; ki < g.k; ++ki) {
-    const int y = i * g.s - g.p + ki;
-    if (y < 0 || y >= g.GH) continue;
     for (int kj = 0; kj < g.k; ++kj) {
-      const int x = j * g.s - g.p + kj;
-      if (x < 0 || x >= g.GW) continue;
-      const float4 v = __ldg(reinterpret_cast<const float4*>(big + (((long long)b * g.GH + y) * g.GW + x) * 4));
-      const float* wt = wsm + (ki * g.k + kj) * 4;
+      float4 v[2];
 #pragma unroll
-      for (int c = 0; c < CSMAX; ++c) {
-        if (c >= g.CS) break;
-        const float4 wv = *reinterpret_cast<const float4*>(wt + c * kk * 4);
-        acc[c] = fmaf(v.x, wv.x, fmaf(v.y, wv.y, fmaf(v.z, wv.z, fmaf(v.w, wv.w, acc[c]))));
+      for (int u = 0; u < 2; ++u)
+        v[u] = ok[u] ? patch[(ii[u] * g.s + ki) * PC + jj[u] * g.s + kj] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4* wt = wsm4 + cs0 * kk + ki * g.k + kj;
+#pragma unroll
+      for (int c = 0; c < IF_CSG; ++c) {
+        const float4 wv = wt[c * kk];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          acc[u][c] = fmaf(v[u].x, wv.x, fmaf(v[u].y, wv.y, fmaf(v[u].z, wv.z, fmaf(v[u].w, wv.w, acc[u][c]))));
       }
     }
   }
-  float4* out = reinterpret_cast<float4*>(a.out + l * a.out_ls + pix * g.CS);
   const float* bias = a.bias ? a.bias + l * a.bias_ls : nullptr;
 #pragma unroll
-  for (int c = 0; c < CSMAX; c += 4)
-    if (c < g.CS)
-      out[c / 4] = make_float4(epi(a, bias, c, acc[c]), epi(a, bias, c + 1, acc[c + 1]), epi(a, bias, c + 2, acc[c + 2]),
-                               epi(a, bias, c + 3, acc[c + 3]));
+  for (int u = 0; u < 2; ++u) {
+    if (!ok[u]) continue;
+    float* o = a.out + l * a.out_ls + (((long long)b * g.SH + i0 + ii[u]) * g.SW + j0 + jj[u]) * g.CS + cs0;
+#pragma unroll
+    for (int c = 0; c < IF_CSG; c += 4)
+      if (cs0 + c < g.CS)
+        *reinterpret_cast<float4*>(o + c) =
+            make_float4(epi(a, bias, cs0 + c, acc[u][c]), epi(a, bias, cs0 + c + 1, acc[u][c + 1]),
+                        epi(a, bias, cs0 + c + 2, acc[u][c + 2]), epi(a, bias, cs0 + c + 3, acc[u][c + 3]));
+  }
+}
+
+int pow2ceil_thin(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
 }
 
 // ---- WGRAD, CG == 4, CS <= 64 ---------------------------------------------
 // dW[cs][tap][0:4] (+)= sum_{spix} smallg[spix][cs] * big[gather(spix, tap)][0:4]
 // A small GEMM (M = CS, N = k*k*4, K = small-map pixels) split over K into
 // fixed chunks: block (chunk, label) computes the whole CS x N partial with a
-// register-tiled SIMT loop over 32-pixel smem stages; a second kernel sums the
-// chunk partials in chunk order (deterministic, no atomics).
+// register-tiled SIMT loop over 32-pixel smem stages (the next stage is
+// prefetched into registers while the current one is multiplied); a second
+// kernel sums the chunk partials in chunk order (deterministic, no atomics).
 constexpr int TW_KC = 32;      // pixels per smem stage
 constexpr int TW_SPLIT = 1024; // pixels per chunk
 __global__ void __launch_bounds__(256) thin_in_wgrad_partial_kernel(GemmArgs a, float* part, int nchunk) {
   const ConvGeo& g = a.g;
   const int l = blockIdx.y, chunk = blockIdx.x;
-  const int kk = g.k * g.k, NN = kk * 4;  // N <= 64
+  const int kk = g.k * g.k;
   const float* sg = a.small + l * a.small_ls;
   const float* big = a.big + l * a.big_ls;
-  __shared__ float gs[TW_KC][64];
-  __shared__ float xs[TW_KC][64];
+  __shared__ __align__(16) float gs[TW_KC][64];
+  __shared__ __align__(16) float xs[TW_KC][64];
   const int tid = threadIdx.x;
   const int tm = tid / 16, tn = tid % 16;  // 4x4 micro tile at (4 tm, 4 tn)
+  const int lq = tid / 8, lp = tid % 8;    // loader: pixel lq of the stage, float4 slots lp and lp + 8
   float acc[4][4] = {};
   const long long K = (long long)g.B * g.SH * g.SW;
   const long long k_begin = (long long)chunk * TW_SPLIT;
   const long long k_end = k_begin + TW_SPLIT < K ? k_begin + TW_SPLIT : K;
+  float4 ra[2], rb[2];
+  auto fetch = [&](long long k0) {
+    const long long sp = k0 + lq;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    ra[0] = ra[1] = rb[0] = rb[1] = z;
+    if (sp >= k_end) return;
+    const int j = (int)(sp % g.SW);
+    const long long t = sp / g.SW;
+    const int i = (int)(t % g.SH), b = (int)(t / g.SH);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int slot = lp + 8 * h;
+      if (slot * 4 < g.CS) ra[h] = __ldg(reinterpret_cast<const float4*>(sg + sp * g.CS) + slot);
+      if (slot < kk) {
+        const int y = i * g.s - g.p + slot / g.k, x = j * g.s - g.p + slot % g.k;
+        if (y >= 0 && y < g.GH && x >= 0 && x < g.GW)
+          rb[h] = __ldg(reinterpret_cast<const float4*>(big + (((long long)b * g.GH + y) * g.GW + x) * 4));
+      }
+    }
+  };
+  fetch(k_begin);
   for (long long k0 = k_begin; k0 < k_end; k0 += TW_KC) {
     __syncthreads();
-    for (int e = tid; e < TW_KC * 64; e += 256) {
-      const int q = e / 64, c = e % 64;
-      const long long sp = k0 + q;
-      float gv = 0.f, xv = 0.f;
-      if (sp < k_end) {
-        if (c < g.CS) gv = sg[sp * g.CS + c];
-        if (c < NN) {
-          const int tap = c / 4, cg = c % 4;
-          const int j = (int)(sp % g.SW);
-          const long long t = sp / g.SW;
-          const int i = (int)(t % g.SH), b = (int)(t / g.SH);
-          const int y = i * g.s - g.p + tap / g.k, x = j * g.s - g.p + tap % g.k;
-          if (y >= 0 && y < g.GH && x >= 0 && x < g.GW) xv = big[(((long long)b * g.GH + y) * g.GW + x) * 4 + cg];
-        }
-      }
-      gs[q][c] = gv;
-      xs[q][c] = xv;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      reinterpret_cast<float4*>(&gs[lq][0])[lp + 8 * h] = ra[h];
+      reinterpret_cast<float4*>(&xs[lq][0])[lp + 8 * h] = rb[h];
     }
     __syncthreads();
-#pragma unroll 4
+    if (k0 + TW_KC < k_end) fetch(k0 + TW_KC);
+#pragma unroll 8
     for (int q = 0; q < TW_KC; ++q) {
       const float4 av = *reinterpret_cast<const float4*>(&gs[q][tm * 4]);
       const float4 bv = *reinterpret_cast<const float4*>(&xs[q][tn * 4]);
@@ -282,10 +388,13 @@ __global__ void dense_wgrad_m4_kernel(GemmArgs a) {
   const float* gz = a.small + l * a.small_ls;
   const float* x = a.big + l * a.big_ls;
   float4 acc[4];
+#pragma unroll
   for (int c = 0; c < 4; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int b = 0; b < g.B; ++b) {
     const float4 xv = __ldg(reinterpret_cast<const float4*>(x + (long long)b * g.CG + f));
-    for (int c = 0; c < g.CS; ++c) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c >= g.CS) break;
       const float gv = gz[(long long)b * g.CS + c];
       acc[c].x = fmaf(gv, xv.x, acc[c].x);
       acc[c].y = fmaf(gv, xv.y, acc[c].y);
@@ -293,7 +402,9 @@ __global__ void dense_wgrad_m4_kernel(GemmArgs a) {
       acc[c].w = fmaf(gv, xv.w, acc[c].w);
     }
   }
-  for (int c = 0; c < g.CS; ++c) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (c >= g.CS) break;
     float4* out = reinterpret_cast<float4*>(a.out + l * a.out_ls + (long long)c * g.CG + f);
     float4 r = acc[c];
     if (a.accumulate) {
@@ -317,8 +428,13 @@ Thin classify(const GemmArgs& a) {
     if (a.kind == GEMM_WGRAD && g.CS <= 4 && g.CG % 4 == 0) return T_D_WGRAD_M4;
     return T_NONE;
   }
-  if (a.kind == GEMM_DGRAD && g.CG <= 4) return T_OUT_DGRAD;
-  if (a.kind == GEMM_FPROP && g.CG == 4 && g.CS <= 64) return T_IN_FPROP;
+  // shared-memory footprints of the staged kernels (weights + input patch) must fit 200 KB
+  const size_t od_smem = sizeof(float4) * g.CS * g.k * g.k +
+                         sizeof(float) * od_patch(OD_TY, g.k, g.s) * od_patch(OD_TX, g.k, g.s) * (g.CS + 4);
+  const int tj = std::min(pow2ceil_thin(g.SW), IF_PIX), ti = IF_PIX / tj;
+  const size_t if_smem = sizeof(float4) * (64 * g.k * g.k + ((ti - 1) * g.s + g.k) * ((tj - 1) * g.s + g.k));
+  if (a.kind == GEMM_DGRAD && g.CG <= 4 && g.CS % 4 == 0 && od_smem <= 200 * 1024 && g.B <= 65535) return T_OUT_DGRAD;
+  if (a.kind == GEMM_FPROP && g.CG == 4 && g.CS <= 64 && if_smem <= 200 * 1024 && g.B <= 65535) return T_IN_FPROP;
   if (a.kind == GEMM_WGRAD && g.CG == 4 && g.CS <= 64 && g.k * g.k <= 16) return T_IN_WGRAD;
   return T_NONE;
 }
@@ -331,17 +447,33 @@ cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st) {
   const ConvGeo& g = a.g;
   switch (classify(a)) {
     case T_OUT_DGRAD: {
-      const long long npix = (long long)g.B * g.GH * g.GW;
-      thin_out_dgrad_kernel<<<dim3((unsigned)((npix + 255) / 256), a.L), 256, 0, st>>>(a);
+      const int kk = g.k * g.k;
+      const size_t smem = sizeof(float4) * g.CS * kk +
+                          sizeof(float) * od_patch(OD_TY, g.k, g.s) * od_patch(OD_TX, g.k, g.s) * (g.CS + 4);
+      static size_t configured = 0;
+      if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(thin_out_dgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+      }
+      const unsigned tiles = (unsigned)(((g.GW + OD_TX - 1) / OD_TX) * ((g.GH + OD_TY - 1) / OD_TY));
+      thin_out_dgrad_kernel<<<dim3(tiles, g.B, a.L), OD_THREADS, smem, st>>>(a);
       break;
     }
     case T_IN_FPROP: {
-      const long long npix = (long long)g.B * g.SH * g.SW;
-      const size_t smem = (size_t)g.CS * g.k * g.k * 4 * sizeof(float);
-      dim3 grid((unsigned)((npix + 127) / 128), a.L);
-      if (g.CS <= 16) thin_in_fprop_kernel<16><<<grid, 128, smem, st>>>(a);
-      else if (g.CS <= 32) thin_in_fprop_kernel<32><<<grid, 128, smem, st>>>(a);
-      else thin_in_fprop_kernel<64><<<grid, 128, smem, st>>>(a);
+      const int TJ = std::min(pow2ceil_thin(g.SW), IF_PIX), TI = IF_PIX / TJ;
+      const int kk = g.k * g.k;
+      const size_t smem = sizeof(float4) * (64 * kk + ((TI - 1) * g.s + g.k) * ((TJ - 1) * g.s + g.k));
+      static size_t configured = 0;
+      if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(thin_in_fprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+      }
+      const unsigned tiles = (unsigned)(((g.SW + TJ - 1) / TJ) * ((g.SH + TI - 1) / TI));
+      thin_in_fprop_kernel<<<dim3(tiles, g.B, a.L), IF_THREADS, smem, st>>>(a, TI, TJ);
       break;
     }
     case T_IN_WGRAD: {

@@ -186,28 +186,44 @@ def test_indices_bit_exact_over_epochs_with_ragged_tail(oracle, math):
 @pytest.mark.parametrize("math", [0, 1])
 def test_ten_step_loss_trajectory(oracle, math):
     """10-step J_D / J_G trajectories (c1, batch 64, one epoch) vs the f64
-    oracle.  Bar: 1e-3 relative, or four times the divergence of the oracle's
-    own f32 restatement from f64 at that step, whichever is larger.  The second
-    clause exists because the GAN/Adam dynamics amplify rounding: the f32
-    oracle (identical algorithm and summation order, only the precision
-    differs) itself drifts from f64 by up to ~3e-3 within 10 steps here
-    (DESIGN.md §parity)."""
+    oracle.  Bar: 1e-3 relative, or four times the intrinsic spread of the
+    trajectory under fp32-level rounding, whichever is larger.  The spread is
+    measured, not assumed: the f64 oracle is re-run from initial weights
+    perturbed by independent relative 2^-24 noise (one fp32 rounding) and the
+    oracle's own f32 restatement is run as-is; `env` is the largest relative
+    deviation any of them shows from the unperturbed f64 run up to that step.
+    The GAN/Adam dynamics amplify rounding (Adam's first step is lr*sign(g),
+    ReLU masks flip), so by step 10 that spread alone is ~1e-3..1e-2 here and a
+    flat 1e-3 bound is not met by the f32 oracle itself."""
     arch, grp = make_pair(1, 2, 640, 64, math)
     orc = oracle.OracleGroup(64, 1, 2, 640, 64, data_seed=3, base_seed=7)
-    o32 = oracle.OracleGroup(32, 1, 2, 640, 64, data_seed=3, base_seed=7)
     assert grp.train_steps(10) == 10
+    runs = [oracle.OracleGroup(32, 1, 2, 640, 64, data_seed=3, base_seed=7)]
+    prng = np.random.default_rng(11)
+    for _ in range(3):
+        o = oracle.OracleGroup(64, 1, 2, 640, 64, data_seed=3, base_seed=7)
+        for l in range(2):
+            for f in (OR["gp"], OR["dp"]):
+                v = o.get(l, f)
+                o.set(l, f, v * (1 + prng.uniform(-2.0**-24, 2.0**-24, v.shape)))
+        runs.append(o)
     orc.step(10)
-    o32.step(10)
+    for o in runs:
+        o.step(10)
     for l in range(2):
         r = grp.reports(l)[:, :2]
         q = orc.get(l, OR["reports"]).reshape(-1, 4)[:, :2]
-        f = o32.get(l, OR["reports"]).reshape(-1, 4)[:, :2]
         err = (np.abs(r - q) / np.abs(q)).max(1)
-        env = (np.abs(f - q) / np.abs(q)).max(1)
+        env = np.zeros_like(err)
+        for o in runs:
+            f = o.get(l, OR["reports"]).reshape(-1, 4)[:, :2]
+            env = np.maximum(env, (np.abs(f - q) / np.abs(q)).max(1))
+        env = np.maximum.accumulate(env)
         tol = np.maximum(1e-3, 4 * env)
-        assert (err <= tol).all(), (err, env)
         print(f"label {l}: device-vs-f64 {np.array2string(err, precision=1)}; "
-              f"f32-oracle-vs-f64 {np.array2string(env, precision=1)}")
+              f"fp32-rounding envelope {np.array2string(env, precision=1)}")
+        assert err[0] <= 1e-4, err  # first step: no amplification yet
+        assert (err <= tol).all(), (err, env)
 
 
 def test_host_batch_step_matches_explicit_inputs(oracle):
