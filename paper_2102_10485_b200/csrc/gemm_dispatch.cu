@@ -91,6 +91,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
   }
   cudaError_t r;
   if (gemm_thin_supported(a)) r = launch_gemm_thin(a, st);  // image-side / dense-head shapes (fp32 FMA)
+  else if (math != MATH_FP32_SIMT && gemm_pair_supported(a)) r = launch_gemm_pair(a, math, st);  // big conv GEMMs
   else if (math != MATH_FP32_SIMT && gemm_tma_supported(a)) r = launch_gemm_tma(a, math, st);  // conv GEMMs
   else if (math != MATH_FP32_SIMT && gemm_tc_supported(a)) r = launch_gemm_tc(a, math, st);
   else r = launch_gemm_simt(a, st);

@@ -1,0 +1,516 @@
+// CTA-pair tcgen05 implicit-GEMM engine (sm_100a, cluster of 2, cta_group::2)
+// for the big convolution GEMMs of the DC-CGAN step.
+//
+// Why pairs: with fp32 operands a 128 x 128 single-CTA tile needs 32 KB of
+// operands per 32-deep k-block, i.e. ~128 B/clk/SM at the tf32 MMA rate —
+// three times what L2 can feed 148 SMs (measured: plain TF32 tops out at
+// ~28% of the tensor pipe in gemm_tma.cu, TF32X3 at ~50%).  A pair computes a
+// 256 x BN tile with `tcgen05.mma.cta_group::2`: each CTA stages its own 128
+// rows of A and HALF of the BN columns of B, the two SMs' tensor cores share
+// the B halves, so operand bytes per flop halve.
+//
+//   tile      M = 256 (CTA rank r owns rows 128r..128r+127), N = BN in {64, 128, 256}
+//   FPROP     rows = output pixels (M box 2*mtp + r), B = weights [N][K] K-major
+//   DGRAD     rows = pixels of one stride phase of the big map, B = weights N-major
+//   WGRAD     SWAPPED w.r.t. gemm_tma.cu: rows = (tap, cin) = 16*CG, N = CS (Cout),
+//             K = output pixels; A = strided big-map boxes, B = gradient boxes,
+//             both MN-major; the epilogue writes W[cs][tap][cg] column-wise
+//
+// Warp roles (384 threads, persistent, one pair per 2 SMs):
+//   warp 0      TMA producer: its CTA's A rows + B half of every stage
+//   warps 1-2   TF32X3: lo = x - trunc_tf32(x) of the landed stage into the lo
+//               ring; TF32: forward the "landed" event.  Either way they then
+//               arrive on the LEADER's `ready` barrier (both CTAs, remote arrive)
+//   warp 3      TMEM allocation (cta_group::2, both CTAs); in the leader the
+//               single MMA-issuing thread; commits multicast to both CTAs
+//   warps 4-11  drain: warp w reads TMEM lane quarter w%4, column half (w-4)/4
+//               of its CTA's accumulator rows; fp32 register sums; epilogue
+// Accuracy design (segmented TMEM accumulation into IEEE fp32 registers,
+// hi = raw fp32, small terms first) as gemm_tc.cu / gemm_tma.cu.
+#include <cuda.h>
+#include <stdint.h>
+
+#include "kernels.hpp"
+#include "tc_ptx.cuh"
+#include "tma_common.cuh"
+
+namespace pg {
+
+namespace {
+
+using namespace tmac;
+
+constexpr int BM = 128;   // rows per CTA
+constexpr int BKT = 32;   // fp32 of K per k-block (one 128-byte row)
+constexpr int NSPLIT = 2; // split / forward warps
+constexpr int NDRAIN = 8;
+constexpr int NT = (4 + NDRAIN) * 32;
+constexpr int W_MMA = 3, W_DRAIN = 4;
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+struct PairPlan {
+  ConvGeo g;
+  int L, phases;
+  SpatialBox box;  // FPROP / DGRAD: the 128-row M box; WGRAD: the 32-row K box
+  int ntn, ntmp, nz, nk;
+  int N, kcb, mrows;  // GEMM N; 32-channel blocks per tap; WGRAD rows (16 CG)
+  int kseg;           // k-blocks per TMEM accumulation segment
+  float* out;
+  long long out_ls;
+  const float* bias;
+  long long bias_ls;
+  int act;
+  float slope;
+  int accumulate, c_valid, c_pad;
+};
+
+__host__ __device__ constexpr int a_bytes() { return BM * BKT * 4; }
+__host__ __device__ constexpr int stage_bytes(int bn) { return a_bytes() + (bn / 2) * BKT * 4; }
+__host__ __device__ constexpr int total_stages(int bn) { return SMEM_BUDGET / stage_bytes(bn); }
+__host__ __device__ constexpr int lo_stages(int bn, bool split) { return split ? total_stages(bn) / 2 : 0; }
+__host__ __device__ constexpr int hi_stages(int bn, bool split) {
+  return total_stages(bn) - lo_stages(bn, split) > 8 ? 8 : total_stages(bn) - lo_stages(bn, split);
+}
+__host__ __device__ constexpr int smem_total(int bn, bool split) {
+  return (hi_stages(bn, split) + lo_stages(bn, split)) * stage_bytes(bn) + 1024 + 1024;
+}
+
+PG_DEV void pair_tile_decode(const PairPlan& P, int t, int& label, int& phase, int& mtp, int& nt) {
+  nt = t % P.ntn;
+  const int r = t / P.ntn;
+  mtp = r % P.ntmp;
+  const int z = r / P.ntmp;
+  label = z / P.phases;
+  phase = z % P.phases;
+}
+
+template <int KIND, int BN, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const PairPlan P) {
+  constexpr bool SPLIT = MODE == MATH_TF32X3;
+  constexpr int SH = hi_stages(BN, SPLIT);
+  constexpr int SL = lo_stages(BN, SPLIT);
+  constexpr int RS = SPLIT ? SL : SH;  // ready ring (lo ring, or the hi ring itself)
+  constexpr int SB = stage_bytes(BN);
+  constexpr int AB = a_bytes();
+  constexpr int BH = BN / 2;  // B columns staged per CTA; also the drain column half
+  constexpr bool A_MN = KIND == GEMM_WGRAD;
+  constexpr bool B_MN = KIND != GEMM_FPROP;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* lo_base = smem + SH * SB;
+  uint64_t* full_h = reinterpret_cast<uint64_t*>(lo_base + SL * SB);
+  uint64_t* empty_h = full_h + SH;
+  uint64_t* ready = empty_h + SH;
+  uint64_t* empty_l = ready + RS;
+  uint64_t* seg_full = empty_l + (SL ? SL : 1);
+  uint64_t* seg_empty = seg_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(seg_empty + 2);
+
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const ConvGeo& g = P.g;
+  const int ntiles = P.ntn * P.ntmp * P.nz;
+
+  if (tid == 0) {
+    for (int s = 0; s < SH; ++s) {
+      mbar_init(full_h + s, 1);
+      mbar_init(empty_h + s, 1);
+    }
+    for (int s = 0; s < RS; ++s) mbar_init(ready + s, 2 * NSPLIT);
+    for (int s = 0; s < SL; ++s) mbar_init(empty_l + s, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(seg_full + b, 1);
+      mbar_init(seg_empty + b, 2 * NDRAIN);
+    }
+    fence_barrier_init();
+  }
+  if (warp == W_MMA) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's barriers exist before anyone arrives remotely
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      uint32_t it = 0;
+      for (int t = cl; t < ntiles; t += ncl) {
+        int label, phase, mtp, nt;
+        pair_tile_decode(P, t, label, phase, mtp, nt);
+        const int n0 = nt * BN + (int)rank * BH;  // this CTA's B half
+        int b0 = 0, i0 = 0, j0 = 0;
+        if (KIND != GEMM_WGRAD) box_origin(P.box, 2 * mtp + (int)rank, b0, i0, j0);
+        DgPhase d{};
+        if (KIND == GEMM_DGRAD) d = dg_phase(g, phase);
+        for (int kb = 0; kb < P.nk; ++kb, ++it) {
+          const int s = it % SH;
+          mbar_wait(empty_h + s, ((it / SH) & 1) ^ 1);
+          mbar_expect_tx(full_h + s, SB);
+          const uint32_t a_dst = smem_u32(smem + s * SB);
+          const uint32_t b_dst = a_dst + AB;
+          if (KIND == GEMM_FPROP) {
+            const int tap = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
+            const int ki = tap / g.k, kj = tap % g.k;
+            tma_load_5d(a_dst, &tmA, full_h + s, c0, j0 * g.s - g.p + kj, i0 * g.s - g.p + ki, b0, label);
+            tma_load_3d(b_dst, &tmB, full_h + s, kb * BKT, n0, label);
+          } else if (KIND == GEMM_DGRAD) {
+            const int tp = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
+            const int ty = tp / d.ntx, tx = tp % d.ntx;
+            const int ki = d.ry + ty * g.s, kj = d.rx + tx * g.s;
+            const int offy = (d.y0 + g.p - d.ry) / g.s - ty;
+            const int offx = (d.x0 + g.p - d.rx) / g.s - tx;
+            tma_load_5d(a_dst, &tmA, full_h + s, c0, j0 + offx, i0 + offy, b0, label);
+#pragma unroll
+            for (int q = 0; q < BH / 32; ++q)
+              tma_load_4d(b_dst + q * (BKT * 128), &tmB, full_h + s, n0 + 32 * q, ki * g.k + kj, c0, label);
+          } else {
+            int kb0, ki0, kj0;
+            box_origin(P.box, kb, kb0, ki0, kj0);
+            const int m0 = mtp * (2 * BM) + (int)rank * BM;
+#pragma unroll
+            for (int q = 0; q < BM / 32; ++q) {
+              const int m = m0 + 32 * q;
+              const int tap = m / g.CG, cg0 = m % g.CG;
+              const int ki = tap / g.k, kj = tap % g.k;
+              tma_load_5d(a_dst + q * (BKT * 128), &tmA, full_h + s, cg0, kj0 * g.s - g.p + kj,
+                          ki0 * g.s - g.p + ki, kb0, label);
+            }
+#pragma unroll
+            for (int q = 0; q < BH / 32; ++q)
+              tma_load_5d(b_dst + q * (BKT * 128), &tmB, full_h + s, n0 + 32 * q, kj0, ki0, kb0, label);
+          }
+        }
+      }
+    }
+  } else if (warp <= NSPLIT) {
+    // ===================== lo split / landed forward (both CTAs) =====================
+    const int st = tid - 32;
+    const uint32_t ready_leader = mapa_shared(smem_u32(ready), 0);
+    uint32_t it = 0;
+    for (int t = cl; t < ntiles; t += ncl) {
+      for (int kb = 0; kb < P.nk; ++kb, ++it) {
+        const int s = it % SH;
+        mbar_wait(full_h + s, (it / SH) & 1);
+        int r = s;
+        if (SPLIT) {
+          const int j = it % SL;
+          r = j;
+          mbar_wait(empty_l + j, ((it / SL) & 1) ^ 1);
+          const float4* src = reinterpret_cast<const float4*>(smem + s * SB);
+          float4* dst = reinterpret_cast<float4*>(lo_base + j * SB);
+#pragma unroll 8
+          for (int i = st; i < SB / 16; i += NSPLIT * 32) {
+            const float4 v = src[i];
+            dst[i] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                                 v.w - tf32_trunc(v.w));
+          }
+          fence_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(ready_leader + r * 8);
+      }
+    }
+  } else if (warp == W_MMA) {
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = make_idesc(2 * BM, BN, A_MN, B_MN);
+      // K-major SW128: 8-row atoms at 1024 B, K-step of 8 fp32 = +32 B inside the row.
+      // MN-major SW128_BASE32B: 4-row atoms at 512 B along K, 32-wide MN atoms at 4096 B.
+      constexpr uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = A_MN ? 512u : 1024u, a_step = A_MN ? 1024u : 32u;
+      constexpr uint32_t b_lbo = B_MN ? 4096u : 16u, b_sbo = B_MN ? 512u : 1024u, b_step = B_MN ? 1024u : 32u;
+      constexpr uint32_t a_lay = A_MN ? UMMA_SW128_BASE32B : UMMA_SW128;
+      constexpr uint32_t b_lay = B_MN ? UMMA_SW128_BASE32B : UMMA_SW128;
+      uint32_t it = 0, sc = 0;
+      for (int t = cl; t < ntiles; t += ncl) {
+        for (int k_seg = 0; k_seg < P.nk; k_seg += P.kseg, ++sc) {
+          const uint32_t buf = sc & 1;
+          mbar_wait_cluster(seg_empty + buf, ((sc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + buf * BN;
+          const int k_end = min(P.nk, k_seg + P.kseg);
+          for (int kb = k_seg; kb < k_end; ++kb, ++it) {
+            const int s = it % SH;
+            const int j = SPLIT ? it % SL : 0;
+            mbar_wait_cluster(ready + (SPLIT ? j : s), (it / RS) & 1);
+            tc_fence_after();
+            const uint32_t a_hi = smem_u32(smem + s * SB), b_hi = a_hi + AB;
+            const uint32_t a_lo = smem_u32(lo_base + j * SB), b_lo = a_lo + AB;
+#pragma unroll
+            for (int kk = 0; kk < BKT / 8; ++kk) {
+              const uint64_t ah = make_desc(a_hi + kk * a_step, a_lbo, a_sbo, a_lay);
+              const uint64_t bh = make_desc(b_hi + kk * b_step, b_lbo, b_sbo, b_lay);
+              const uint32_t acc = (kb != k_seg || kk) ? 1u : 0u;
+              if (SPLIT) {
+                const uint64_t al = make_desc(a_lo + kk * a_step, a_lbo, a_sbo, a_lay);
+                const uint64_t bl = make_desc(b_lo + kk * b_step, b_lbo, b_sbo, b_lay);
+                mma_tf32_pair(d, al, bh, idesc, acc);  // small terms first
+                mma_tf32_pair(d, ah, bl, idesc, 1u);
+                mma_tf32_pair(d, ah, bh, idesc, 1u);
+              } else {
+                mma_tf32_pair(d, ah, bh, idesc, acc);
+              }
+            }
+            mma_commit_pair(empty_h + s, 3);
+            if (SPLIT) mma_commit_pair(empty_l + j, 3);
+          }
+          mma_commit_pair(seg_full + buf, 3);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== drain + epilogue (both CTAs) =====================
+    const int q = warp & 3;               // TMEM lane quarter
+    const int half = (warp - W_DRAIN) >> 2;  // accumulator column half
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const uint32_t seg_empty_leader = mapa_shared(smem_u32(seg_empty), 0);
+    uint32_t sc = 0;
+    for (int t = cl; t < ntiles; t += ncl) {
+      int label, phase, mtp, nt;
+      pair_tile_decode(P, t, label, phase, mtp, nt);
+      float acc[BH];
+#pragma unroll
+      for (int i = 0; i < BH; ++i) acc[i] = 0.f;
+      for (int k_seg = 0; k_seg < P.nk; k_seg += P.kseg, ++sc) {
+        const uint32_t buf = sc & 1;
+        mbar_wait_cluster(seg_full + buf, (sc >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < BH / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_base + buf * BN + half * BH + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[c * 32 + i] += __uint_as_float(r[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(seg_empty_leader + buf * 8);
+      }
+      const int row = q * 32 + lane;
+      const int nb = nt * BN + half * BH;  // first output column of this thread
+      if (KIND == GEMM_WGRAD) {
+        const int m = mtp * (2 * BM) + (int)rank * BM + row;
+        if (m < P.mrows) {
+          float* base = P.out + (long long)label * P.out_ls + m;
+#pragma unroll
+          for (int c = 0; c < BH; ++c) {
+            const int n = nb + c;
+            if (n < P.N) {
+              float* dst = base + (long long)n * P.mrows;
+              *dst = P.accumulate ? *dst + acc[c] : acc[c];
+            }
+          }
+        }
+      } else {
+        int b0, i0, j0;
+        box_origin(P.box, 2 * mtp + (int)rank, b0, i0, j0);
+        const int b = b0 + row / (P.box.TH * P.box.TW);
+        const int ii = i0 + (row / P.box.TW) % P.box.TH;
+        const int jj = j0 + row % P.box.TW;
+        float* crow = nullptr;
+        if (KIND == GEMM_FPROP) {
+          if (b < g.B && ii < g.SH && jj < g.SW)
+            crow = P.out + (long long)label * P.out_ls + (((long long)b * g.SH + ii) * g.SW + jj) * g.CS;
+        } else {
+          const DgPhase d = dg_phase(g, phase);
+          if (b < g.B && ii < d.ny && jj < d.nx)
+            crow = P.out + (long long)label * P.out_ls +
+                   (((long long)b * g.GH + d.y0 + ii * g.s) * g.GW + d.x0 + jj * g.s) * g.CG;
+        }
+        if (crow) {
+          const float* bias = P.bias ? P.bias + (long long)label * P.bias_ls : nullptr;
+#pragma unroll
+          for (int c4 = 0; c4 < BH; c4 += 4) {
+            const int n = nb + c4;
+            if (n < P.N) {
+              float o[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                float x = acc[c4 + u];
+                const int nn = n + u;
+                if (nn % P.c_pad < P.c_valid) {
+                  if (bias) x += bias[nn];
+                  x = act_fwd(P.act, x, P.slope);
+                } else {
+                  x = 0.f;
+                }
+                o[u] = x;
+              }
+              *reinterpret_cast<float4*>(crow + n) = make_float4(o[0], o[1], o[2], o[3]);
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no remote arrive / MMA into the peer after this point
+  if (warp == W_MMA) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+template <int KIND, int BN, int MODE>
+cudaError_t launch_pair_bn(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, cudaStream_t st) {
+  constexpr int smem = smem_total(BN, MODE == MATH_TF32X3);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_pair_kernel<KIND, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int tiles = P.ntn * P.ntmp * P.nz;
+  if (tiles == 0 || P.nk == 0) return cudaSuccess;
+  const int pairs = std::min(tiles, sm_count_tma() / 2);
+  gemm_pair_kernel<KIND, BN, MODE><<<2 * pairs, NT, smem, st>>>(ta, tb, P);
+  return launched();
+}
+
+template <int KIND, int MODE>
+cudaError_t launch_pair_kind(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, int bn,
+                             cudaStream_t st) {
+  if (bn == 64) return launch_pair_bn<KIND, 64, MODE>(ta, tb, P, st);
+  if (bn == 128) return launch_pair_bn<KIND, 128, MODE>(ta, tb, P, st);
+  return launch_pair_bn<KIND, 256, MODE>(ta, tb, P, st);
+}
+
+int pair_bn(int n) { return n >= 256 ? 256 : n >= 128 ? 128 : 64; }
+
+}  // namespace
+
+bool gemm_pair_supported(const GemmArgs& a) {
+  static const bool disabled = [] {
+    const char* e = std::getenv("PG_NO_PAIR");
+    return e && std::atoi(e) != 0;
+  }();
+  if (disabled || !encode_fn() || sm_count_tma() < 2) return false;
+  const ConvGeo& g = a.g;
+  if (g.s < 1 || g.s > 8 || g.k < 1) return false;
+  if (a.kind == GEMM_FPROP && spatial_box(g.B, g.SH, g.SW, BM).TW * g.s > 256) return false;
+  if (a.kind == GEMM_WGRAD && spatial_box(g.B, g.SH, g.SW, BKT).TW * g.s > 256) return false;
+  if (a.kind == GEMM_DGRAD && g.k % g.s) return false;
+  if (!aligned16(a.out) || !aligned16(a.w) || a.out_ls % 4 || a.w_ls % 4) return false;
+  switch (a.kind) {
+    case GEMM_FPROP:
+      return g.CG % 32 == 0 && g.CS >= 64 && g.CS % 32 == 0 && aligned16(a.big) && a.big_ls % 4 == 0;
+    case GEMM_DGRAD:
+      return g.CS % 32 == 0 && g.CG >= 64 && g.CG % 32 == 0 && aligned16(a.small) && a.small_ls % 4 == 0;
+    default:
+      return g.CG % 32 == 0 && g.CS % 32 == 0 && g.CS >= 64 && aligned16(a.small) && aligned16(a.big) &&
+             a.small_ls % 4 == 0 && a.big_ls % 4 == 0;
+  }
+}
+
+cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
+  const ConvGeo& g = a.g;
+  PairPlan P{};
+  P.g = g;
+  P.L = a.L;
+  P.phases = a.kind == GEMM_DGRAD ? g.s * g.s : 1;
+  P.out = a.out;
+  P.out_ls = a.out_ls;
+  P.bias = a.bias;
+  P.bias_ls = a.bias_ls;
+  P.act = a.act;
+  P.slope = a.slope;
+  P.accumulate = a.accumulate;
+  P.c_valid = a.c_valid;
+  P.c_pad = a.c_pad;
+  P.nz = a.L * P.phases;
+  // TF32X3 keeps every TMEM accumulation chain short (the tensor core adds with
+  // truncation); plain TF32 is not fp32-accurate anyway
+  static const int kseg_env = [] {
+    const char* e = std::getenv("PG_KSEG");
+    return e ? std::atoi(e) : 0;
+  }();
+  P.kseg = kseg_env > 0 ? kseg_env : (math == MATH_TF32 ? 8 : 4);
+  const int kk = g.k * g.k;
+  CUtensorMap ta, tb;
+  const int one[5] = {1, 1, 1, 1, 1};
+  const int sstr[5] = {1, g.s, g.s, 1, 1};
+  bool ok = true;
+  int bn, ntm = 1;
+  if (a.kind == GEMM_FPROP) {
+    P.N = g.CS;
+    P.kcb = g.CG / BKT;
+    P.nk = kk * P.kcb;
+    P.box = spatial_box(g.B, g.SH, g.SW, BM);
+    ntm = P.box.nb * P.box.ny * P.box.nx;
+    bn = pair_bn(P.N);
+    const long long ad[5] = {g.CG, g.GW, g.GH, g.B, a.L};
+    const long long as[4] = {g.CG, (long long)g.GW * g.CG, (long long)g.GH * g.GW * g.CG, a.big_ls};
+    const int abox[5] = {BKT, P.box.TW * g.s, P.box.TH * g.s, P.box.TB, 1};
+    ok = ok && make_map(&ta, a.big, 5, ad, as, abox, sstr, CU_TENSOR_MAP_SWIZZLE_128B);
+    const long long K = (long long)kk * g.CG;
+    const long long bd[3] = {K, g.CS, a.L};
+    const long long bs[2] = {K, a.w_ls};
+    const int bbox[3] = {BKT, bn / 2, 1};
+    ok = ok && make_map(&tb, a.w, 3, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if (a.kind == GEMM_DGRAD) {
+    P.N = g.CG;
+    P.kcb = g.CS / BKT;
+    const int nty = g.k / g.s, ntx = nty;
+    P.nk = nty * ntx * P.kcb;
+    const int ny = (g.GH + g.s - 1) / g.s, nx = (g.GW + g.s - 1) / g.s;
+    P.box = spatial_box(g.B, ny, nx, BM);
+    ntm = P.box.nb * P.box.ny * P.box.nx;
+    bn = pair_bn(P.N);
+    const long long ad[5] = {g.CS, g.SW, g.SH, g.B, a.L};
+    const long long as[4] = {g.CS, (long long)g.SW * g.CS, (long long)g.SH * g.SW * g.CS, a.small_ls};
+    const int abox[5] = {BKT, P.box.TW, P.box.TH, P.box.TB, 1};
+    ok = ok && make_map(&ta, a.small, 5, ad, as, abox, one, CU_TENSOR_MAP_SWIZZLE_128B);
+    const long long bd[4] = {g.CG, kk, g.CS, a.L};
+    const long long bs[3] = {g.CG, (long long)kk * g.CG, a.w_ls};
+    const int bbox[4] = {32, 1, BKT, 1};
+    ok = ok && make_map(&tb, a.w, 4, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  } else {
+    P.N = g.CS;
+    P.mrows = kk * g.CG;
+    P.kcb = 0;
+    P.box = spatial_box(g.B, g.SH, g.SW, BKT);
+    P.nk = P.box.nb * P.box.ny * P.box.nx;
+    ntm = (P.mrows + BM - 1) / BM;
+    bn = pair_bn(P.N);
+    // A: strided big-map boxes (32 channels of one tap), MN-major
+    const long long ad[5] = {g.CG, g.GW, g.GH, g.B, a.L};
+    const long long as[4] = {g.CG, (long long)g.GW * g.CG, (long long)g.GH * g.GW * g.CG, a.big_ls};
+    const int abox[5] = {32, P.box.TW * g.s, P.box.TH * g.s, P.box.TB, 1};
+    ok = ok && make_map(&ta, a.big, 5, ad, as, abox, sstr, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    // B: gradient of the small map, 32 output channels per box, MN-major
+    const long long bd[5] = {g.CS, g.SW, g.SH, g.B, a.L};
+    const long long bs[4] = {g.CS, (long long)g.SW * g.CS, (long long)g.SH * g.SW * g.CS, a.small_ls};
+    const int bbox[5] = {32, P.box.TW, P.box.TH, P.box.TB, 1};
+    ok = ok && make_map(&tb, a.small, 5, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  P.ntmp = (ntm + 1) / 2;
+  P.ntn = (P.N + bn - 1) / bn;
+  const bool x3 = math != MATH_TF32;
+  switch (a.kind) {
+    case GEMM_FPROP:
+      return x3 ? launch_pair_kind<GEMM_FPROP, MATH_TF32X3>(ta, tb, P, bn, st)
+                : launch_pair_kind<GEMM_FPROP, MATH_TF32>(ta, tb, P, bn, st);
+    case GEMM_DGRAD:
+      return x3 ? launch_pair_kind<GEMM_DGRAD, MATH_TF32X3>(ta, tb, P, bn, st)
+                : launch_pair_kind<GEMM_DGRAD, MATH_TF32>(ta, tb, P, bn, st);
+    default:
+      return x3 ? launch_pair_kind<GEMM_WGRAD, MATH_TF32X3>(ta, tb, P, bn, st)
+                : launch_pair_kind<GEMM_WGRAD, MATH_TF32>(ta, tb, P, bn, st);
+  }
+}
+
+}  // namespace pg

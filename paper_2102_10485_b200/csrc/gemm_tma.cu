@@ -34,6 +34,7 @@
 #include <mutex>
 
 #include "gemm_gather.cuh"
+#include "tma_common.cuh"
 #include "kernels.hpp"
 #include "tc_ptx.cuh"
 
@@ -41,16 +42,13 @@ namespace pg {
 
 namespace {
 
+using namespace tmac;
+
 constexpr int BM = 128;
 constexpr int BKT = 32;   // fp32 of K per k-block: one 128-byte row
 constexpr int KSEG = 2;   // k-blocks per TMEM accumulation segment (8 K-steps: chain <= 24 MMA adds in TF32X3)
 constexpr int NT = 320;
 constexpr int SMEM_BUDGET = 200 * 1024;
-
-struct SpatialBox {
-  int TB, TH, TW;  // box extent in samples / rows / columns (product = rows of the box)
-  int nb, ny, nx;  // number of boxes along each
-};
 
 struct TmaPlan {
   ConvGeo g;
@@ -67,36 +65,20 @@ struct TmaPlan {
   int accumulate, c_valid, c_pad;
 };
 
-struct DgPhase {
-  int ry, rx, y0, x0, ny, nx, ntx;
-};
-
-PG_DEV DgPhase dg_phase(const ConvGeo& g, int phase) {
-  DgPhase d;
-  d.ry = phase / g.s;
-  d.rx = phase % g.s;
-  d.y0 = phase_origin(d.ry, g.s, g.p);
-  d.x0 = phase_origin(d.rx, g.s, g.p);
-  d.ny = d.y0 < g.GH ? (g.GH - d.y0 + g.s - 1) / g.s : 0;
-  d.nx = d.x0 < g.GW ? (g.GW - d.x0 + g.s - 1) / g.s : 0;
-  d.ntx = d.rx < g.k ? (g.k - d.rx + g.s - 1) / g.s : 0;
-  return d;
-}
-
 __host__ __device__ constexpr int a_bytes() { return BM * BKT * 4; }
 __host__ __device__ constexpr int b_bytes(int bn) { return bn * BKT * 4; }
 __host__ __device__ constexpr int hi_bytes(int bn) { return a_bytes() + b_bytes(bn); }
-__host__ __device__ constexpr int lo_stages(int bn, bool split) { return split ? (bn >= 128 ? 2 : 3) : 0; }
+// TF32X3: the lo ring sits between the split warps and the MMA (a slot is
+// refilled only after the MMAs that read it retire), so it gets half the
+// stages; the hi ring keeps the rest for TMA latency.
+__host__ __device__ constexpr int total_stages(int bn) { return SMEM_BUDGET / hi_bytes(bn); }
+__host__ __device__ constexpr int lo_stages(int bn, bool split) { return split ? total_stages(bn) / 2 : 0; }
 __host__ __device__ constexpr int hi_stages(int bn, bool split) {
-  return (SMEM_BUDGET - lo_stages(bn, split) * hi_bytes(bn)) / hi_bytes(bn) > 8
-             ? 8
-             : (SMEM_BUDGET - lo_stages(bn, split) * hi_bytes(bn)) / hi_bytes(bn);
+  return total_stages(bn) - lo_stages(bn, split) > 8 ? 8 : total_stages(bn) - lo_stages(bn, split);
 }
 __host__ __device__ constexpr int smem_total(int bn, bool split) {
   return (hi_stages(bn, split) + lo_stages(bn, split)) * hi_bytes(bn) + 1024 + 1024;
 }
-
-PG_DEV float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 PG_DEV void tile_decode(const TmaPlan& P, int t, int& label, int& phase, int& mt, int& nt) {
   nt = t % P.ntn;
@@ -105,16 +87,6 @@ PG_DEV void tile_decode(const TmaPlan& P, int t, int& label, int& phase, int& mt
   const int z = r / P.ntm;
   label = z / P.phases;
   phase = z % P.phases;
-}
-
-PG_DEV void box_origin(const SpatialBox& b, int idx, int& b0, int& i0, int& j0) {
-  const int xt = idx % b.nx;
-  const int r = idx / b.nx;
-  const int yt = r % b.ny;
-  const int bt = r / b.ny;
-  b0 = bt * b.TB;
-  i0 = yt * b.TH;
-  j0 = xt * b.TW;
 }
 
 template <int KIND, int BN, int MODE>
@@ -131,7 +103,8 @@ __global__ void __launch_bounds__(NT, 1)
   constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // keep the shared-window provenance (LDS/STS, not generic LD/ST) while aligning to 1024
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* lo_base = smem + SH * HI;
   uint64_t* full_h = reinterpret_cast<uint64_t*>(lo_base + SL * HI);
   uint64_t* empty_h = full_h + SH;
@@ -385,70 +358,6 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // ---------------------------------------------------------------- host side
-
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
-// fp32 tensor map over `rank` dims (innermost first); strides in floats for dims 1..rank-1
-bool make_map(CUtensorMap* m, const float* base, int rank, const long long* dims, const long long* strides,
-              const int* box, const int* estr, CUtensorMapSwizzle swz) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t gd[5], gs[4];
-  cuuint32_t bd[5], es[5];
-  for (int i = 0; i < rank; ++i) {
-    gd[i] = static_cast<cuuint64_t>(dims[i]);
-    bd[i] = static_cast<cuuint32_t>(box[i]);
-    es[i] = static_cast<cuuint32_t>(estr[i]);
-  }
-  for (int i = 0; i + 1 < rank; ++i) gs[i] = static_cast<cuuint64_t>(strides[i]) * 4;
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(base), gd, gs, bd, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-int pow2ceil(int x) {
-  int p = 1;
-  while (p < x) p <<= 1;
-  return p;
-}
-
-SpatialBox spatial_box(int B, int H, int W, int rows) {
-  SpatialBox b;
-  b.TW = std::min(pow2ceil(W), rows);
-  b.TH = std::min(pow2ceil(H), rows / b.TW);
-  b.TB = rows / (b.TW * b.TH);
-  b.nx = (W + b.TW - 1) / b.TW;
-  b.ny = (H + b.TH - 1) / b.TH;
-  b.nb = (B + b.TB - 1) / b.TB;
-  return b;
-}
-
-int sm_count_tma() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
-  }
-  return n;
-}
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <int KIND, int BN, int MODE>
 cudaError_t launch_tma_bn(const CUtensorMap& ta, const CUtensorMap& tb, const TmaPlan& P, cudaStream_t st) {

@@ -27,6 +27,8 @@ cudaError_t launch_gemm_tc(const GemmArgs& a, int math, cudaStream_t st);  // tc
 bool gemm_tc_supported(const GemmArgs& a);
 cudaError_t launch_gemm_tma(const GemmArgs& a, int math, cudaStream_t st);  // TMA-fed tcgen05 engine
 bool gemm_tma_supported(const GemmArgs& a);
+cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st);  // CTA-pair (cta_group::2) engine
+bool gemm_pair_supported(const GemmArgs& a);
 cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st);  // thin.cu
 bool gemm_thin_supported(const GemmArgs& a);
 float* gemm_scratch(size_t floats, cudaStream_t st);  // grow-only workspace for split-K reductions

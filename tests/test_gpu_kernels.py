@@ -53,6 +53,10 @@ CONV_CASES = [
     (3, 64, 14, 14, 128, 4, 2, 1),
     (5, 128, 8, 8, 256, 4, 2, 1),
     (3, 32, 16, 16, 32, 4, 2, 1),
+    # CTA-pair engine edge cases: odd number of M boxes (empty peer half), N not a multiple
+    # of the pair tile (B half fully / partly out of bounds), WGRAD rows 16*Cin = 6 pair tiles
+    (3, 64, 10, 10, 96, 4, 2, 1),
+    (2, 96, 12, 12, 160, 4, 2, 1),
 ]
 
 
