@@ -7,9 +7,11 @@ or does not load, every entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpartgan_b200.so"
+LIB_PATH = Path(os.environ.get("PG_LIB", "")) if os.environ.get("PG_LIB") else \
+    Path(__file__).resolve().parent / "_lib" / "libpartgan_b200.so"  # PG_LIB: tuning-variant builds only
 
 PG_OK, PG_EINVAL, PG_ECUDA, PG_ENONFINITE, PG_EUNSUPPORTED = 0, -1, -2, -3, -4
 MATH_FP32_SIMT, MATH_TF32X3, MATH_TF32 = 0, 1, 2

@@ -16,15 +16,17 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
-OBJ = PKG / "_lib" / "obj"
-LIB = PKG / "_lib" / "libpartgan_b200.so"
+# PG_VARIANT=name PG_NVCC_DEFS="-DX=1 ..." builds a tuning variant into _lib/<name>/ (load it with PG_LIB)
+VARIANT = os.environ.get("PG_VARIANT", "")
+OBJ = PKG / "_lib" / (f"{VARIANT}/obj" if VARIANT else "obj")
+LIB = PKG / "_lib" / (f"{VARIANT}/libpartgan_b200.so" if VARIANT else "libpartgan_b200.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("PG_CXX", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CCBIN = ["-ccbin", CXX]
 NVFLAGS = ARCH + CCBIN + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-                  "-Xptxas", "-O3", f"-I{INCLUDE}"]
+                  "-Xptxas", "-O3", f"-I{INCLUDE}"] + os.environ.get("PG_NVCC_DEFS", "").split()
 # host code is compiled without FP contraction so host-side arithmetic (dataset
 # generation, init) is bit-identical to the CPU oracle's
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread", "-Wall", "-Wno-unused-parameter",

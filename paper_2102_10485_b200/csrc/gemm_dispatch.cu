@@ -1,6 +1,7 @@
 // Engine selection for the implicit GEMMs, launch accounting and the
 // optional per-GEMM event timing used by bench.py's roofline figure.
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <mutex>
@@ -16,6 +17,13 @@ std::atomic<bool> g_timing{false};
 std::mutex g_mu;
 std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
 std::vector<std::string> g_tags;
+bool lowered_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PG_NO_LOWERED");
+    return !(e && std::atoi(e) != 0);
+  }();
+  return on;
+}
 }  // namespace
 
 std::string gemm_timing_report() {
@@ -90,7 +98,8 @@ cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
     cudaEventRecord(e0, st);
   }
   cudaError_t r;
-  if (gemm_thin_supported(a)) r = launch_gemm_thin(a, st);  // image-side / dense-head shapes (fp32 FMA)
+  if (math != MATH_FP32_SIMT && lowered_enabled() && gemm_lowered_supported(a)) r = launch_gemm_lowered(a, math, st);
+  else if (gemm_thin_supported(a)) r = launch_gemm_thin(a, st);  // image-side / dense-head shapes (fp32 FMA)
   else if (math != MATH_FP32_SIMT && gemm_pair_supported(a)) r = launch_gemm_pair(a, math, st);  // big conv GEMMs
   else if (math != MATH_FP32_SIMT && gemm_tma_supported(a)) r = launch_gemm_tma(a, math, st);  // conv GEMMs
   else if (math != MATH_FP32_SIMT && gemm_tc_supported(a)) r = launch_gemm_tc(a, math, st);

@@ -47,6 +47,9 @@ constexpr int NDRAIN = 8;
 constexpr int NT = (4 + NDRAIN) * 32;
 constexpr int W_MMA = 3, W_DRAIN = 4;
 constexpr int SMEM_BUDGET = 200 * 1024;
+#ifndef PG_PAIR_SL
+#define PG_PAIR_SL 0
+#endif
 
 struct PairPlan {
   ConvGeo g;
@@ -67,7 +70,10 @@ struct PairPlan {
 __host__ __device__ constexpr int a_bytes() { return BM * BKT * 4; }
 __host__ __device__ constexpr int stage_bytes(int bn) { return a_bytes() + (bn / 2) * BKT * 4; }
 __host__ __device__ constexpr int total_stages(int bn) { return SMEM_BUDGET / stage_bytes(bn); }
-__host__ __device__ constexpr int lo_stages(int bn, bool split) { return split ? total_stages(bn) / 2 : 0; }
+// Equal hi and lo rings (lo slot j == hi slot s): measured 1.4-1.6x faster on
+// the BN = 64 / 128 tiles than one stage more on either side (PG_PAIR_SL = +-1,
+// scripts/gemm_sweep.py with tuning-variant builds).
+__host__ __device__ constexpr int lo_stages(int bn, bool split) { return split ? (bn >= 256 ? 3 : total_stages(bn) / 2 + PG_PAIR_SL) : 0; }
 __host__ __device__ constexpr int hi_stages(int bn, bool split) {
   return total_stages(bn) - lo_stages(bn, split) > 8 ? 8 : total_stages(bn) - lo_stages(bn, split);
 }

@@ -29,6 +29,8 @@ cudaError_t launch_gemm_tma(const GemmArgs& a, int math, cudaStream_t st);  // T
 bool gemm_tma_supported(const GemmArgs& a);
 cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st);  // CTA-pair (cta_group::2) engine
 bool gemm_pair_supported(const GemmArgs& a);
+cudaError_t launch_gemm_lowered(const GemmArgs& a, int math, cudaStream_t st);  // im2col / col2im + pair engine
+bool gemm_lowered_supported(const GemmArgs& a);
 cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st);  // thin.cu
 bool gemm_thin_supported(const GemmArgs& a);
 float* gemm_scratch(size_t floats, cudaStream_t st);  // grow-only workspace for split-K reductions
