@@ -61,6 +61,16 @@ struct ConvGeo {
 // WGRAD: C[cs][tap][cg] (+)= sum_{spix} smallg[spix][cs] * big[gather(spix,tap)][cg]   (weight gradients)
 enum GemmKind : int { GEMM_FPROP = 0, GEMM_DGRAD = 1, GEMM_WGRAD = 2 };
 
+// Per-channel statistics fused into the FPROP / DGRAD epilogue (CTA-pair
+// engine; gemm_stat_slots() says whether a GEMM supports it and how many
+// 32-row slots it writes).  stat layout: [L][slots][4][N].
+//   STAT_FWD     out = z (act must be NONE): {shift, sum(z-shift), sum((z-shift)^2), rows}
+//                per slot, shift = the slot's first row (merged with Chan's formula)
+//   STAT_BWD_BN  out = g1 = act_bwd(gemm, y) written instead of the raw gradient:
+//                {sum g1, sum g1 (z-mu), sum (z-mu), 0}   (BatchNorm backward sums)
+//   STAT_BWD_ACT out = g1 = act_bwd(gemm, y): {sum g1, 0, 0, 0}   (bias gradient)
+enum StatMode : int { STAT_NONE = 0, STAT_FWD = 1, STAT_BWD_BN = 2, STAT_BWD_ACT = 3 };
+
 struct GemmArgs {
   int kind;
   ConvGeo g;
@@ -75,6 +85,13 @@ struct GemmArgs {
   float slope;
   int accumulate;      // WGRAD: out += result
   int c_valid, c_pad;  // FPROP/DGRAD: output column n is padding (written 0) iff n % c_pad >= c_valid
+  int stat_mode;       // StatMode (FPROP / DGRAD on the pair engine only)
+  float* stat;
+  const float* stat_y;   // BWD: activation output map, same layout and label stride as out
+  const float* stat_z;   // BWD_BN: pre-BatchNorm map, same layout and label stride as out
+  const float* stat_mu;  // BWD_BN: batch mean [L][N]
+  int stat_act;
+  float stat_slope;
 };
 
 // phase decomposition of the big map along one axis for stride s, pad p:

@@ -62,10 +62,80 @@ __global__ void channel_reduce_kernel(ChannelMap cm, int mode, const float* __re
 }
 
 PG_DEV float sum_partials(const ChannelMap& cm, const float* partial, int l, int k, int c) {
-  const int nchunk = (cm.R + RED_ROWS - 1) / RED_ROWS;
+  const int nchunk = cm.nslot > 0 ? cm.nslot : (cm.R + RED_ROWS - 1) / RED_ROWS;
+  const int pk = cm.nslot > 0 ? 4 : 3;
   float t = 0.f;
-  for (int ch = 0; ch < nchunk; ++ch) t += partial[(((long long)l * nchunk + ch) * 3 + k) * cm.Cp + c];
+  for (int ch = 0; ch < nchunk; ++ch) t += partial[(((long long)l * nchunk + ch) * pk + k) * cm.Cp + c];
   return t;
+}
+
+// Per-slot {shift, sum d, sum d^2, n} (d = z - shift) -> mean / M2 merged with
+// Chan's formula in f64; var is the biased variance over all rows
+// (network.cpp:171-184), running stats as bn_finalize_var.  Block = 32
+// channels x 8 slot lanes: lane j merges slots j, j+8, ... in order, then lane 0
+// merges the 8 lane results in order (deterministic, independent of timing).
+struct Moments {
+  double n, mu, m2;
+};
+PG_DEV void chan_merge(Moments& a, double nb, double mb, double m2b) {
+  if (nb <= 0.0) return;
+  const double nt = a.n + nb, delta = mb - a.mu;
+  a.mu += delta * nb / nt;
+  a.m2 += m2b + delta * delta * a.n * nb / nt;
+  a.n = nt;
+}
+
+__global__ void bn_stats_finalize_kernel(ChannelMap cm, const float* stat, float* mean, float* istd, float* running,
+                                         long long run_ls, float eps, float mom, int update) {
+  const int l = blockIdx.y, c = blockIdx.x * 32 + threadIdx.x, j = threadIdx.y;
+  __shared__ Moments sm[8][32];
+  Moments a{0.0, 0.0, 0.0};
+  if (c < cm.Cp) {
+    for (int s = j; s < cm.nslot; s += 8) {
+      const float* e = stat + ((long long)l * cm.nslot + s) * 4 * cm.Cp + c;
+      const double nb = e[3 * cm.Cp];
+      if (nb <= 0.0) continue;
+      const double s1 = e[cm.Cp], s2 = e[2 * cm.Cp];
+      chan_merge(a, nb, (double)e[0] + s1 / nb, fmax(s2 - s1 * s1 / nb, 0.0));
+    }
+  }
+  sm[j][threadIdx.x] = a;
+  __syncthreads();
+  if (j != 0 || c >= cm.Cp) return;
+  for (int k = 1; k < 8; ++k) chan_merge(a, sm[k][threadIdx.x].n, sm[k][threadIdx.x].mu, sm[k][threadIdx.x].m2);
+  const int i = l * cm.Cp + c;
+  const double var = a.n > 0.0 ? a.m2 / a.n : 0.0;
+  mean[i] = (float)a.mu;
+  istd[i] = 1.f / sqrtf((float)var + eps);
+  if (update && c < cm.C) {
+    float* rm = running + (long long)l * run_ls;
+    float* rv = rm + cm.C;
+    const float m = (float)cm.R;
+    const float unbias = m > 1.f ? m / (m - 1.f) : 1.f;
+    rm[c] = (1.f - mom) * rm[c] + mom * (float)a.mu;
+    rv[c] = (1.f - mom) * rv[c] + mom * (float)var * unbias;
+  }
+}
+
+// [L][nslot][4][Cp] slot sums -> [L][1][4][Cp] (entries 0..2), fixed order
+__global__ void slot_sum_kernel(ChannelMap cm, const float* stat, float* out) {
+  const int l = blockIdx.y, c = blockIdx.x * 32 + threadIdx.x, j = threadIdx.y;
+  __shared__ float sm[3][8][33];
+  float t[3] = {0.f, 0.f, 0.f};
+  if (c < cm.Cp)
+    for (int s = j; s < cm.nslot; s += 8) {
+      const float* e = stat + ((long long)l * cm.nslot + s) * 4 * cm.Cp + c;
+      t[0] += e[0];
+      t[1] += e[cm.Cp];
+      t[2] += e[2 * cm.Cp];
+    }
+  for (int k = 0; k < 3; ++k) sm[k][j][threadIdx.x] = t[k];
+  __syncthreads();
+  if (j < 3 && c < cm.Cp) {
+    float r = 0.f;
+    for (int k = 0; k < 8; ++k) r += sm[j][k][threadIdx.x];
+    out[((long long)l * 4 + j) * cm.Cp + c] = r;
+  }
 }
 
 __global__ void bn_finalize_mean_kernel(ChannelMap cm, const float* partial, float* mean) {
@@ -189,7 +259,7 @@ __global__ void bn_bwd_apply_kernel(ChannelMap cm, const float* __restrict__ gy,
     const long long o = (long long)l * cm.ls + q * 4;
     const int c0 = (int)((q * 4) % cm.Cp);
     float4 g4 = *reinterpret_cast<const float4*>(gy + o);
-    float4 y4 = *reinterpret_cast<const float4*>(y + o);
+    float4 y4 = act == ACT_NONE ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(y + o);
     float4 x4 = *reinterpret_cast<const float4*>(x + o);
     float g[4] = {g4.x, g4.y, g4.z, g4.w}, yy[4] = {y4.x, y4.y, y4.z, y4.w}, xx[4] = {x4.x, x4.y, x4.z, x4.w};
     float r[4];
@@ -431,6 +501,21 @@ cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* m
                             const float* gamma_beta, long long gb_ls, int act, float slope, float* y, cudaStream_t st) {
   dim3 grid(grid_for((long long)cm.R * cm.Cp / 4, 256, 4096), cm.L);
   bn_apply_kernel<<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y);
+  return launched();
+}
+
+cudaError_t launch_bn_stats_finalize(const ChannelMap& cm, const float* stat, float* mean, float* istd, float* running,
+                                     long long run_ls, float eps, float momentum, int update_running, cudaStream_t st) {
+  if (cm.nslot <= 0) return cudaErrorInvalidValue;
+  bn_stats_finalize_kernel<<<dim3((cm.Cp + 31) / 32, cm.L), dim3(32, 8), 0, st>>>(cm, stat, mean, istd, running,
+                                                                                  run_ls, eps, momentum,
+                                                                                  update_running);
+  return launched();
+}
+
+cudaError_t launch_slot_sum(const ChannelMap& cm, const float* stat, float* out, cudaStream_t st) {
+  if (cm.nslot <= 0) return cudaErrorInvalidValue;
+  slot_sum_kernel<<<dim3((cm.Cp + 31) / 32, cm.L), dim3(32, 8), 0, st>>>(cm, stat, out);
   return launched();
 }
 

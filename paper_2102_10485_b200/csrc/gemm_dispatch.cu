@@ -17,12 +17,13 @@ std::atomic<bool> g_timing{false};
 std::mutex g_mu;
 std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
 std::vector<std::string> g_tags;
-bool lowered_enabled() {
-  static const bool on = [] {
+// PG_NO_LOWERED bit 1: im2col FPROP, bit 2: column-GEMM + col2im DGRAD (A/B only)
+bool lowered_enabled(const GemmArgs& a) {
+  static const int off = [] {
     const char* e = std::getenv("PG_NO_LOWERED");
-    return !(e && std::atoi(e) != 0);
+    return e ? std::atoi(e) : 0;
   }();
-  return on;
+  return !(off & (a.kind == GEMM_FPROP ? 1 : 2));
 }
 }  // namespace
 
@@ -90,7 +91,15 @@ double gemm_timing_read_ms() {
   return total;
 }
 
+int gemm_stat_slots(const GemmArgs& a, int math) {
+  if (math == MATH_FP32_SIMT) return 0;
+  if (lowered_enabled(a) && gemm_lowered_supported(a)) return gemm_lowered_stat_slots(a);
+  if (gemm_thin_supported(a)) return 0;
+  return gemm_pair_stat_slots(a);
+}
+
 cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
+  if (a.stat_mode != STAT_NONE && gemm_stat_slots(a, math) == 0) return cudaErrorInvalidValue;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {
     cudaEventCreate(&e0);
@@ -98,7 +107,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
     cudaEventRecord(e0, st);
   }
   cudaError_t r;
-  if (math != MATH_FP32_SIMT && lowered_enabled() && gemm_lowered_supported(a)) r = launch_gemm_lowered(a, math, st);
+  if (math != MATH_FP32_SIMT && lowered_enabled(a) && gemm_lowered_supported(a)) r = launch_gemm_lowered(a, math, st);
   else if (gemm_thin_supported(a)) r = launch_gemm_thin(a, st);  // image-side / dense-head shapes (fp32 FMA)
   else if (math != MATH_FP32_SIMT && gemm_pair_supported(a)) r = launch_gemm_pair(a, math, st);  // big conv GEMMs
   else if (math != MATH_FP32_SIMT && gemm_tma_supported(a)) r = launch_gemm_tma(a, math, st);  // conv GEMMs

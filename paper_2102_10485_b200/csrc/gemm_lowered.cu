@@ -133,6 +133,14 @@ bool gemm_lowered_supported(const GemmArgs& a) {
   return false;
 }
 
+int gemm_lowered_stat_slots(const GemmArgs& a) {
+  if (a.kind != GEMM_FPROP) return 0;  // the DGRAD output comes out of col2im
+  const ConvGeo& g = a.g;
+  GemmArgs p = fprop_1x1(a, g.B, g.SH, g.SW, g.k * g.k * 4, g.CS);
+  p.big = p.w = p.out = reinterpret_cast<float*>(256);
+  return gemm_pair_stat_slots(p);
+}
+
 cudaError_t launch_gemm_lowered(const GemmArgs& a, int math, cudaStream_t st) {
   const ConvGeo& g = a.g;
   const int kk = g.k * g.k;
@@ -157,6 +165,13 @@ cudaError_t launch_gemm_lowered(const GemmArgs& a, int math, cudaStream_t st) {
     p.slope = a.slope;
     p.c_valid = a.c_valid;
     p.c_pad = a.c_pad;
+    p.stat_mode = a.stat_mode;  // same output map: the fused statistics carry over
+    p.stat = a.stat;
+    p.stat_y = a.stat_y;
+    p.stat_z = a.stat_z;
+    p.stat_mu = a.stat_mu;
+    p.stat_act = a.stat_act;
+    p.stat_slope = a.stat_slope;
     return launch_gemm_pair(p, math, st);
   }
   // DGRAD: columns P = small . Wt, then the col2im gather

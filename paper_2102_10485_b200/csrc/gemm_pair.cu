@@ -65,7 +65,166 @@ struct PairPlan {
   int act;
   float slope;
   int accumulate, c_valid, c_pad;
+  int stat_mode, nslot;
+  float* stat;
+  const float* stat_y;
+  const float* stat_z;
+  const float* stat_mu;
+  int stat_act;
+  float stat_slope;
 };
+
+// Sum of v[0..7] over the 32 lanes of a warp in 9 shuffles (recursive
+// halving): afterwards lanes 4c..4c+3 hold the total of column red8_col(lane) = c.
+PG_DEV int red8_col(int lane) { return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1); }
+PG_DEV float red8(float (&v)[8], int lane) {
+#pragma unroll
+  for (int w = 4, m = 16; w >= 1; w >>= 1, m >>= 1) {
+    const bool up = lane & m;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w];
+      const float keep = up ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  float r = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 2);
+  return r + __shfl_xor_sync(0xffffffffu, r, 1);
+}
+
+
+// activation derivative through the output for the fused backward modes
+// (ReLU / LeakyReLU / none: branch-free selects; see common.cuh act_bwd)
+PG_DEV float act_bwd_rl(int act, float g, float y, float slope) {
+  const float neg = act == ACT_LRELU ? g * slope : (act == ACT_RELU ? 0.f : g);
+  const bool pos = act == ACT_LRELU ? y >= 0.f : y > 0.f;
+  return act == ACT_NONE || pos ? g : neg;
+}
+
+template <int ACT>
+PG_DEV float act_t(float x, float slope) {
+  if (ACT == ACT_RELU) return x > 0.f ? x : 0.f;
+  if (ACT == ACT_LRELU) return x >= 0.f ? x : x * slope;
+  if (ACT == ACT_TANH) return tanhf(x);
+  if (ACT == ACT_SIGMOID) return 1.f / (expf(-x) + 1.f);
+  return x;
+}
+
+// bias, padding columns (written 0) and activation of one output row
+template <int ACT, int BH>
+PG_DEV void epi_store(const float (&acc)[BH], float* crow, int nb, const float* bias, const PairPlan& P) {
+  const bool padded = P.c_valid != P.c_pad;
+#pragma unroll
+  for (int c4 = 0; c4 < BH; c4 += 4) {
+    const int n = nb + c4;
+    if (n >= P.N) break;
+    float o[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float x = acc[c4 + u];
+      if (bias) x += bias[n + u];
+      x = act_t<ACT>(x, P.slope);
+      if (padded && (n + u) % P.c_pad >= P.c_valid) x = 0.f;
+      o[u] = x;
+    }
+    *reinterpret_cast<float4*>(crow + n) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// output row + per-channel statistics over the warp's 32 rows (StatMode);
+// warp-uniform: every lane runs it, padding rows contribute nothing
+template <int MODE, int BH>
+PG_DEV void epi_stats(const float (&acc)[BH], bool valid, long long lo_off, int nb, const float* bias, float* st,
+                      int label, int lane, const PairPlan& P) {
+  const bool padded = P.c_valid != P.c_pad;
+  const float rows = (float)__popc(__ballot_sync(0xffffffffu, valid));
+  const int col = red8_col(lane);
+#pragma unroll
+  for (int c8 = 0; c8 < BH; c8 += 8) {
+    const int n0 = nb + c8;
+    if (n0 >= P.N) break;
+    float v[8], w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      float x = acc[c8 + u];
+      if (bias) x += bias[n0 + u];
+      if (padded && (n0 + u) % P.c_pad >= P.c_valid) x = 0.f;
+      v[u] = x;
+    }
+    if (MODE != STAT_FWD) {
+#pragma unroll
+      for (int u4 = 0; u4 < 8; u4 += 4) {
+        float4 y4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) y4 = __ldg(reinterpret_cast<const float4*>(P.stat_y + lo_off + n0 + u4));
+        v[u4] = act_bwd_rl(P.stat_act, v[u4], y4.x, P.stat_slope);
+        v[u4 + 1] = act_bwd_rl(P.stat_act, v[u4 + 1], y4.y, P.stat_slope);
+        v[u4 + 2] = act_bwd_rl(P.stat_act, v[u4 + 2], y4.z, P.stat_slope);
+        v[u4 + 3] = act_bwd_rl(P.stat_act, v[u4 + 3], y4.w, P.stat_slope);
+      }
+    }
+    if (valid) {
+      float* crow = P.out + lo_off + n0;
+      *reinterpret_cast<float4*>(crow) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(crow + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    float* s8 = st + n0;
+    if (MODE == STAT_FWD) {
+      // shifted sums around the slot's first row (lane 0), merged across slots
+      // with Chan's formula by bn_stats_finalize
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float sh = __shfl_sync(0xffffffffu, v[u], 0);
+        if (lane == 0) s8[u] = sh;
+        v[u] = valid ? v[u] - sh : 0.f;
+        w[u] = v[u] * v[u];
+      }
+      const float s1 = red8(v, lane);
+      const float s2 = red8(w, lane);
+      if (!(lane & 3)) {
+        s8[P.N + col] = s1;
+        s8[2 * P.N + col] = s2;
+        s8[3 * P.N + col] = rows;
+      }
+    } else if (MODE == STAT_BWD_BN) {
+      const float* mu = P.stat_mu + (long long)label * P.N + n0;
+      float t[8];
+#pragma unroll
+      for (int u4 = 0; u4 < 8; u4 += 4) {
+        float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) z4 = __ldg(reinterpret_cast<const float4*>(P.stat_z + lo_off + n0 + u4));
+        w[u4] = valid ? z4.x - mu[u4] : 0.f;
+        w[u4 + 1] = valid ? z4.y - mu[u4 + 1] : 0.f;
+        w[u4 + 2] = valid ? z4.z - mu[u4 + 2] : 0.f;
+        w[u4 + 3] = valid ? z4.w - mu[u4 + 3] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (!valid) v[u] = 0.f;
+        t[u] = v[u] * w[u];
+      }
+      const float s1 = red8(v, lane);
+      const float s2 = red8(t, lane);
+      const float s3 = red8(w, lane);
+      if (!(lane & 3)) {
+        s8[col] = s1;
+        s8[P.N + col] = s2;
+        s8[2 * P.N + col] = s3;
+        s8[3 * P.N + col] = 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (!valid) v[u] = 0.f;
+      const float s1 = red8(v, lane);
+      if (!(lane & 3)) {
+        s8[col] = s1;
+        s8[P.N + col] = 0.f;
+        s8[2 * P.N + col] = 0.f;
+        s8[3 * P.N + col] = 0.f;
+      }
+    }
+  }
+}
 
 __host__ __device__ constexpr int a_bytes() { return BM * BKT * 4; }
 __host__ __device__ constexpr int stage_bytes(int bn) { return a_bytes() + (bn / 2) * BKT * 4; }
@@ -90,7 +249,10 @@ PG_DEV void pair_tile_decode(const PairPlan& P, int t, int& label, int& phase, i
   phase = z % P.phases;
 }
 
-template <int KIND, int BN, int MODE>
+// TMEM accumulation buffers (segments in flight between the MMA and the drain)
+__host__ __device__ constexpr int seg_bufs(int bn) { return 512 / bn > 4 ? 4 : 512 / bn; }
+
+template <int KIND, int BN, int MODE, bool STATS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const PairPlan P) {
@@ -103,7 +265,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   constexpr int BH = BN / 2;  // B columns staged per CTA; also the drain column half
   constexpr bool A_MN = KIND == GEMM_WGRAD;
   constexpr bool B_MN = KIND != GEMM_FPROP;
-  constexpr uint32_t TMEM_COLS = 2 * BN;
+  constexpr int NB = seg_bufs(BN);
+  constexpr uint32_t TMEM_COLS = NB * BN;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -113,8 +276,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   uint64_t* ready = empty_h + SH;
   uint64_t* empty_l = ready + RS;
   uint64_t* seg_full = empty_l + (SL ? SL : 1);
-  uint64_t* seg_empty = seg_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(seg_empty + 2);
+  uint64_t* seg_empty = seg_full + NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(seg_empty + NB);
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const uint32_t rank = cluster_ctarank();
@@ -129,7 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     }
     for (int s = 0; s < RS; ++s) mbar_init(ready + s, 2 * NSPLIT);
     for (int s = 0; s < SL; ++s) mbar_init(empty_l + s, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(seg_full + b, 1);
       mbar_init(seg_empty + b, 2 * NDRAIN);
     }
@@ -237,8 +400,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       uint32_t it = 0, sc = 0;
       for (int t = cl; t < ntiles; t += ncl) {
         for (int k_seg = 0; k_seg < P.nk; k_seg += P.kseg, ++sc) {
-          const uint32_t buf = sc & 1;
-          mbar_wait_cluster(seg_empty + buf, ((sc >> 1) & 1) ^ 1);
+          const uint32_t buf = sc % NB;
+          mbar_wait_cluster(seg_empty + buf, ((sc / NB) & 1) ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + buf * BN;
           const int k_end = min(P.nk, k_seg + P.kseg);
@@ -286,8 +449,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 #pragma unroll
       for (int i = 0; i < BH; ++i) acc[i] = 0.f;
       for (int k_seg = 0; k_seg < P.nk; k_seg += P.kseg, ++sc) {
-        const uint32_t buf = sc & 1;
-        mbar_wait_cluster(seg_full + buf, (sc >> 1) & 1);
+        const uint32_t buf = sc % NB;
+        mbar_wait_cluster(seg_full + buf, (sc / NB) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < BH / 32; ++c) {
@@ -322,38 +485,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         const int b = b0 + row / (P.box.TH * P.box.TW);
         const int ii = i0 + (row / P.box.TW) % P.box.TH;
         const int jj = j0 + row % P.box.TW;
-        float* crow = nullptr;
+        long long off = -1;  // this row's offset in the output map (per label), -1 = padding row
         if (KIND == GEMM_FPROP) {
-          if (b < g.B && ii < g.SH && jj < g.SW)
-            crow = P.out + (long long)label * P.out_ls + (((long long)b * g.SH + ii) * g.SW + jj) * g.CS;
+          if (b < g.B && ii < g.SH && jj < g.SW) off = (((long long)b * g.SH + ii) * g.SW + jj) * g.CS;
         } else {
           const DgPhase d = dg_phase(g, phase);
           if (b < g.B && ii < d.ny && jj < d.nx)
-            crow = P.out + (long long)label * P.out_ls +
-                   (((long long)b * g.GH + d.y0 + ii * g.s) * g.GW + d.x0 + jj * g.s) * g.CG;
+            off = (((long long)b * g.GH + d.y0 + ii * g.s) * g.GW + d.x0 + jj * g.s) * g.CG;
         }
-        if (crow) {
-          const float* bias = P.bias ? P.bias + (long long)label * P.bias_ls : nullptr;
-#pragma unroll
-          for (int c4 = 0; c4 < BH; c4 += 4) {
-            const int n = nb + c4;
-            if (n < P.N) {
-              float o[4];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                float x = acc[c4 + u];
-                const int nn = n + u;
-                if (nn % P.c_pad < P.c_valid) {
-                  if (bias) x += bias[nn];
-                  x = act_fwd(P.act, x, P.slope);
-                } else {
-                  x = 0.f;
-                }
-                o[u] = x;
-              }
-              *reinterpret_cast<float4*>(crow + n) = make_float4(o[0], o[1], o[2], o[3]);
+        const bool valid = off >= 0;
+        const float* bias = P.bias ? P.bias + (long long)label * P.bias_ls : nullptr;
+        if (!STATS) {
+          if (valid) {
+            float* crow = P.out + (long long)label * P.out_ls + off;
+            // one specialised copy per activation: the executed epilogue stays
+            // small (the kernel is instruction-cache sensitive)
+            switch (P.act) {
+              case ACT_RELU: epi_store<ACT_RELU, BH>(acc, crow, nb, bias, P); break;
+              case ACT_LRELU: epi_store<ACT_LRELU, BH>(acc, crow, nb, bias, P); break;
+              case ACT_TANH: epi_store<ACT_TANH, BH>(acc, crow, nb, bias, P); break;
+              case ACT_SIGMOID: epi_store<ACT_SIGMOID, BH>(acc, crow, nb, bias, P); break;
+              default: epi_store<ACT_NONE, BH>(acc, crow, nb, bias, P); break;
             }
           }
+          continue;
+        }
+        const long long lo_off = (long long)label * P.out_ls + (valid ? off : 0);
+        float* st = P.stat + ((long long)label * P.nslot + ((phase * P.ntmp + mtp) * 2 + (int)rank) * 4 + q) * 4 * P.N;
+        switch (P.stat_mode) {
+          case STAT_FWD: epi_stats<STAT_FWD, BH>(acc, valid, lo_off, nb, bias, st, label, lane, P); break;
+          case STAT_BWD_BN: epi_stats<STAT_BWD_BN, BH>(acc, valid, lo_off, nb, bias, st, label, lane, P); break;
+          default: epi_stats<STAT_BWD_ACT, BH>(acc, valid, lo_off, nb, bias, st, label, lane, P); break;
         }
       }
     }
@@ -369,21 +531,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
 
 // ---------------------------------------------------------------- host side
 
-template <int KIND, int BN, int MODE>
-cudaError_t launch_pair_bn(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, cudaStream_t st) {
+template <int KIND, int BN, int MODE, bool STATS>
+cudaError_t launch_pair_st(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, int grid,
+                           cudaStream_t st) {
   constexpr int smem = smem_total(BN, MODE == MATH_TF32X3);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_pair_kernel<KIND, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel<KIND, BN, MODE, STATS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  gemm_pair_kernel<KIND, BN, MODE, STATS><<<grid, NT, smem, st>>>(ta, tb, P);
+  return launched();
+}
+
+template <int KIND, int BN, int MODE>
+cudaError_t launch_pair_bn(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, cudaStream_t st) {
   const int tiles = P.ntn * P.ntmp * P.nz;
   if (tiles == 0 || P.nk == 0) return cudaSuccess;
   const int pairs = std::min(tiles, sm_count_tma() / 2);
-  gemm_pair_kernel<KIND, BN, MODE><<<2 * pairs, NT, smem, st>>>(ta, tb, P);
-  return launched();
+  if (KIND != GEMM_WGRAD && P.stat_mode != STAT_NONE)
+    return launch_pair_st<KIND, BN, MODE, KIND != GEMM_WGRAD>(ta, tb, P, 2 * pairs, st);
+  return launch_pair_st<KIND, BN, MODE, false>(ta, tb, P, 2 * pairs, st);
 }
 
 template <int KIND, int MODE>
@@ -421,6 +591,19 @@ bool gemm_pair_supported(const GemmArgs& a) {
   }
 }
 
+int gemm_pair_stat_slots(const GemmArgs& a) {
+  const ConvGeo& g = a.g;
+  if (a.kind == GEMM_WGRAD || !gemm_pair_supported(a)) return 0;
+  if (a.kind == GEMM_FPROP) {
+    const SpatialBox b = spatial_box(g.B, g.SH, g.SW, BM);
+    if (g.CS % 8) return 0;
+    return (b.nb * b.ny * b.nx + 1) / 2 * 8;
+  }
+  const SpatialBox b = spatial_box(g.B, (g.GH + g.s - 1) / g.s, (g.GW + g.s - 1) / g.s, BM);
+  if (g.CG % 8) return 0;
+  return g.s * g.s * ((b.nb * b.ny * b.nx + 1) / 2) * 8;
+}
+
 cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   const ConvGeo& g = a.g;
   PairPlan P{};
@@ -436,6 +619,13 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   P.accumulate = a.accumulate;
   P.c_valid = a.c_valid;
   P.c_pad = a.c_pad;
+  P.stat_mode = a.kind == GEMM_WGRAD ? STAT_NONE : a.stat_mode;
+  P.stat = a.stat;
+  P.stat_y = a.stat_y;
+  P.stat_z = a.stat_z;
+  P.stat_mu = a.stat_mu;
+  P.stat_act = a.stat_act;
+  P.stat_slope = a.stat_slope;
   P.nz = a.L * P.phases;
   // TF32X3 keeps every TMEM accumulation chain short (the tensor core adds with
   // truncation); plain TF32 is not fp32-accurate anyway
@@ -505,6 +695,26 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   if (!ok) return cudaErrorInvalidValue;
   P.ntmp = (ntm + 1) / 2;
   P.ntn = (P.N + bn - 1) / bn;
+  P.nslot = P.phases * P.ntmp * 8;
+  // profiling aid: PG_FORCE_STATS=1 runs plain FPROP/DGRAD launches with STAT_FWD into a private buffer
+  static const bool force_stats = [] {
+    const char* e = std::getenv("PG_FORCE_STATS");
+    return e && std::atoi(e) != 0;
+  }();
+  if (force_stats && a.kind != GEMM_WGRAD && P.stat_mode == STAT_NONE && P.act == ACT_NONE && P.N % 8 == 0) {
+    static float* buf = nullptr;
+    static size_t cap = 0;
+    const size_t need = (size_t)a.L * P.nslot * 4 * P.N;
+    if (need > cap) {
+      cudaStreamSynchronize(st);
+      cudaFree(buf);
+      if (cudaMalloc(&buf, need * sizeof(float)) != cudaSuccess) return cudaErrorMemoryAllocation;
+      cap = need;
+    }
+    P.stat_mode = STAT_FWD;
+    P.stat = buf;
+  }
+  if (P.stat_mode != STAT_NONE && (!P.stat || P.N % 8 || P.act != ACT_NONE)) return cudaErrorInvalidValue;
   const bool x3 = math != MATH_TF32;
   switch (a.kind) {
     case GEMM_FPROP:

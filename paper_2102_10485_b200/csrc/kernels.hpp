@@ -31,6 +31,11 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st);  // 
 bool gemm_pair_supported(const GemmArgs& a);
 cudaError_t launch_gemm_lowered(const GemmArgs& a, int math, cudaStream_t st);  // im2col / col2im + pair engine
 bool gemm_lowered_supported(const GemmArgs& a);
+int gemm_pair_stat_slots(const GemmArgs& a);
+int gemm_lowered_stat_slots(const GemmArgs& a);
+// number of 32-row statistic slots launch_gemm(a, math) writes when a.stat_mode
+// is set (0: the engine chosen for this GEMM cannot fuse statistics)
+int gemm_stat_slots(const GemmArgs& a, int math);
 cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st);  // thin.cu
 bool gemm_thin_supported(const GemmArgs& a);
 float* gemm_scratch(size_t floats, cudaStream_t st);  // grow-only workspace for split-K reductions
@@ -47,6 +52,9 @@ enum ReduceMode : int {
 struct ChannelMap {
   int L, R, Cp, C;         // rows per label, padded / valid channels
   long long ls;            // label stride of the maps (floats)
+  // partials source: 0 = channel_reduce chunks ([L][chunks][3][Cp]); > 0 = that
+  // many GEMM-epilogue statistic slots ([L][slots][4][Cp], see StatMode)
+  int nslot = 0;
 };
 int reduce_chunks(int R);
 size_t reduce_partial_floats(const ChannelMap& cm);
@@ -62,6 +70,12 @@ cudaError_t launch_bn_finalize_var(const ChannelMap& cm, const float* partial, c
 // y = act(gamma (x - mean) istd + beta); eval mode passes running stats as mean/istd source.
 cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* mean, const float* istd,
                             const float* gamma_beta, long long gb_ls, int act, float slope, float* y, cudaStream_t st);
+// BN forward statistics from STAT_FWD epilogue slots (cm.nslot > 0): mean,
+// istd and the running-stat update in one pass (Chan's parallel merge, f64)
+cudaError_t launch_bn_stats_finalize(const ChannelMap& cm, const float* stat, float* mean, float* istd, float* running,
+                                     long long run_ls, float eps, float momentum, int update_running, cudaStream_t st);
+// [L][nslot][4][Cp] epilogue slot sums -> [L][1][4][Cp]; read it back with cm.nslot = 1
+cudaError_t launch_slot_sum(const ChannelMap& cm, const float* stat, float* out, cudaStream_t st);
 // eval-mode: istd from running var
 cudaError_t launch_bn_eval_stats(const ChannelMap& cm, const float* running, long long run_ls, float eps, float* mean,
                                  float* istd, cudaStream_t st);

@@ -315,6 +315,7 @@ DevNet::DevNet(const std::string& spec, const std::vector<long>& in_shape, int L
     long R = static_cast<long>(Bmax_) * b.out.H * b.out.W;
     ChannelMap cm{L_, static_cast<int>(R), static_cast<int>(b.out.Cp), static_cast<int>(b.out.C), 0};
     part = std::max(part, reduce_partial_floats(cm));
+    part = std::max(part, static_cast<size_t>(L_) * 4 * b.out.Cp);  // launch_slot_sum output
     // bias reductions over the linear output map
     ChannelMap cb{L_, static_cast<int>(static_cast<long>(Bmax_) * (b.lin == LK::ConvT ? b.geo.GH * b.geo.GW : b.geo.SH * b.geo.SW)),
                   b.lin == LK::ConvT ? b.geo.CG : b.geo.CS, 0, 0};
@@ -450,7 +451,28 @@ ConvGeo DevNet::geo_for(const Block& b, int B) const {
   return g;
 }
 
+// PG_NO_FUSE bit 1: forward BN statistics, bit 2: backward sums (A/B timing only)
+static bool fuse_enabled(int bit) {
+  static const int off = [] {
+    const char* e = std::getenv("PG_NO_FUSE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return !(off & bit);
+}
+
+float* DevNet::stat_buf(size_t floats, cudaStream_t st) {
+  if (stat_.n < floats) {
+    check_cuda(cudaStreamSynchronize(st), "stat buffer grow");
+    stat_ = DeviceBuf(floats);
+  }
+  return stat_.p;
+}
+
 void DevNet::linear_fwd(const Block& b, int B, const float* x, float* y, bool with_epilogue, cudaStream_t st) {
+  check_cuda(launch_gemm(linear_args(b, B, x, y, with_epilogue), math_, st), "linear forward");
+}
+
+GemmArgs DevNet::linear_args(const Block& b, int B, const float* x, float* y, bool with_epilogue) const {
   GemmArgs a{};
   a.g = geo_for(b, B);
   a.L = L_;
@@ -472,7 +494,7 @@ void DevNet::linear_fwd(const Block& b, int B, const float* x, float* y, bool wi
   a.slope = b.slope;
   a.c_valid = static_cast<int>(b.out.C);
   a.c_pad = static_cast<int>(b.out.Cp);
-  check_cuda(launch_gemm(a, math_, st), "linear forward");
+  return a;
 }
 
 void DevNet::forward(Trace& t, int B, bool train, bool update_running, cudaStream_t st) {
@@ -484,10 +506,25 @@ void DevNet::forward(Trace& t, int B, bool train, bool update_running, cudaStrea
       continue;
     }
     float* z = t.pre[i].p;
-    linear_fwd(b, B, t.act[i], z, false, st);
+    GemmArgs a = linear_args(b, B, t.act[i], z, false);
     ChannelMap cm{L_, static_cast<int>(static_cast<long>(B) * b.out.H * b.out.W), static_cast<int>(b.out.Cp),
                   static_cast<int>(b.out.C), static_cast<long long>(B) * b.out.numel()};
-    if (train) {
+    const int slots = train && fuse_enabled(1) ? gemm_stat_slots(a, math_) : 0;
+    if (slots > 0) {
+      // batch statistics fused into the GEMM epilogue (per 32-row slot), merged here
+      a.stat_mode = STAT_FWD;
+      a.stat = stat_buf(static_cast<size_t>(L_) * slots * 4 * b.out.Cp, st);
+      check_cuda(launch_gemm(a, math_, st), "linear forward");
+      cm.nslot = slots;
+      check_cuda(launch_bn_stats_finalize(cm, a.stat, t.mean[i].p, t.istd[i].p, running.p + b.off_run, Bf_,
+                                          static_cast<float>(b.bn.eps), static_cast<float>(b.bn.momentum),
+                                          update_running ? 1 : 0, st),
+                 "bn stats finalize");
+      cm.nslot = 0;
+    } else {
+      check_cuda(launch_gemm(a, math_, st), "linear forward");
+    }
+    if (train && slots == 0) {
       check_cuda(launch_channel_reduce(cm, RED_SUM, z, nullptr, nullptr, nullptr, 0, 0.f, partial_.p, st), "bn sum");
       check_cuda(launch_bn_finalize_mean(cm, partial_.p, t.mean[i].p, st), "bn mean");
       check_cuda(launch_channel_reduce(cm, RED_SQDEV, z, nullptr, nullptr, t.mean[i].p, 0, 0.f, partial_.p, st), "bn var");
@@ -495,7 +532,7 @@ void DevNet::forward(Trace& t, int B, bool train, bool update_running, cudaStrea
                                         static_cast<float>(b.bn.eps), static_cast<float>(b.bn.momentum),
                                         update_running ? 1 : 0, st),
                  "bn finalize");
-    } else {
+    } else if (!train) {
       check_cuda(launch_bn_eval_stats(cm, running.p + b.off_run, Bf_, static_cast<float>(b.bn.eps), t.mean[i].p,
                                       t.istd[i].p, st),
                  "bn eval stats");
@@ -510,6 +547,7 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
                       cudaStream_t st) {
   const int nb = static_cast<int>(blocks_.size());
   const float* gy = gy_ext;
+  int fused = 0;  // > 0: gy already is act_bwd(gy, y) and its channel sums sit in stat_ (that many slots)
   for (int i = nb - 1; i >= 0; --i) {
     const Block& b = blocks_[static_cast<size_t>(i)];
     const long long out_ls = static_cast<long long>(B) * b.out.numel();
@@ -521,21 +559,38 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
     float* dbias = param_grads ? grads.p + b.off_b : nullptr;
     bool bias_done = false;
     if (b.has_bn) {
-      check_cuda(launch_channel_reduce(cm, RED_BN_BWD, t.pre[i].p, gy, t.act[i + 1], t.mean[i].p, b.act, b.slope,
-                                       partial_.p, st),
-                 "bn bwd reduce");
+      ChannelMap cs = cm;
+      if (fused) {
+        // sums from the producing GEMM's epilogue, pre-reduced over its slots
+        cs.nslot = fused;
+        check_cuda(launch_slot_sum(cs, stat_.p, partial_.p, st), "bn bwd slot sum");
+        cs.nslot = 1;
+      } else {
+        check_cuda(launch_channel_reduce(cm, RED_BN_BWD, t.pre[i].p, gy, t.act[i + 1], t.mean[i].p, b.act, b.slope,
+                                         partial_.p, st),
+                   "bn bwd reduce");
+      }
       bool closed_form_bias = b.bias_per_bn_channel();
-      check_cuda(launch_bn_bwd_finalize(cm, partial_.p, t.istd[i].p, params.p + b.off_bn, P_,
+      check_cuda(launch_bn_bwd_finalize(cs, partial_.p, t.istd[i].p, params.p + b.off_bn, P_,
                                         param_grads ? grads.p + b.off_bn : nullptr, P_,
                                         closed_form_bias ? dbias : nullptr, P_, accumulate ? 1 : 0, 1, coef_.p, st),
                  "bn bwd finalize");
       bias_done = closed_form_bias;
-      check_cuda(launch_bn_bwd_apply(cm, gy, t.act[i + 1], t.pre[i].p, t.mean[i].p, coef_.p, b.act, b.slope, gz_.p, st),
+      check_cuda(launch_bn_bwd_apply(cm, gy, t.act[i + 1], t.pre[i].p, t.mean[i].p, coef_.p, fused ? ACT_NONE : b.act,
+                                     b.slope, gz_.p, st),
                  "bn bwd apply");
       gz = gz_.p;
-    } else if (b.act != ACT_NONE) {
+    } else if (b.act != ACT_NONE && !fused) {
       check_cuda(launch_act_bwd(cm, gy, t.act[i + 1], b.act, b.slope, gz_.p, st), "act bwd");
       gz = gz_.p;
+    }
+    if (param_grads && !bias_done && fused && !b.has_bn) {
+      ChannelMap cb = cm;
+      cb.nslot = fused;
+      check_cuda(launch_slot_sum(cb, stat_.p, partial_.p, st), "bias slot sum");
+      cb.nslot = 1;
+      check_cuda(launch_bias_finalize(cb, partial_.p, dbias, P_, accumulate ? 1 : 0, st), "bias finalize");
+      bias_done = true;
     }
     if (param_grads && !bias_done) {
       // bias gradient = column sums of gz over the linear output rows
@@ -584,6 +639,7 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
     float* gx = nullptr;
     if (i > 0) gx = gscratch_[i % 2].p;
     else gx = gx_ext;
+    fused = 0;
     if (gx) {
       GemmArgs a{};
       a.g = geo_for(b, B);
@@ -603,6 +659,22 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
         a.kind = GEMM_DGRAD;
         a.small = gz;
         a.small_ls = out_ls;
+      }
+      if (i > 0) {
+        // the previous block's activation backward and BatchNorm / bias sums ride
+        // on this GEMM's epilogue when its engine supports it
+        const Block& pb = blocks_[static_cast<size_t>(i - 1)];
+        const int slots = (pb.has_bn || pb.act != ACT_NONE) && fuse_enabled(2) ? gemm_stat_slots(a, math_) : 0;
+        if (slots > 0) {
+          a.stat_mode = pb.has_bn ? STAT_BWD_BN : STAT_BWD_ACT;
+          a.stat = stat_buf(static_cast<size_t>(L_) * slots * 4 * b.in.Cp, st);
+          a.stat_y = t.act[static_cast<size_t>(i)];
+          a.stat_z = pb.has_bn ? t.pre[static_cast<size_t>(i - 1)].p : nullptr;
+          a.stat_mu = pb.has_bn ? t.mean[static_cast<size_t>(i - 1)].p : nullptr;
+          a.stat_act = pb.act;
+          a.stat_slope = pb.slope;
+          fused = slots;
+        }
       }
       check_cuda(launch_gemm(a, math_, st), "dgrad");
     }

@@ -140,10 +140,12 @@ class DevNet {
   std::vector<Block> blocks_;
   long long P_ = 0, Bf_ = 0;
   long ref_P_ = 0, ref_Bf_ = 0;
-  DeviceBuf partial_, coef_, gscratch_[2], gz_;
+  DeviceBuf partial_, coef_, gscratch_[2], gz_, stat_;
 
   ConvGeo geo_for(const Block& b, int B) const;
+  GemmArgs linear_args(const Block& b, int B, const float* x, float* y, bool with_epilogue) const;
   void linear_fwd(const Block& b, int B, const float* x, float* y, bool with_epilogue, cudaStream_t st);
+  float* stat_buf(size_t floats, cudaStream_t st);  // grow-only buffer for fused GEMM statistics
   template <class F>
   void map_params(const Block& b, F f) const;  // f(ref_index, dev_index) for every real parameter
 };

@@ -57,6 +57,8 @@ CONV_CASES = [
     # of the pair tile (B half fully / partly out of bounds), WGRAD rows 16*Cin = 6 pair tiles
     (3, 64, 10, 10, 96, 4, 2, 1),
     (2, 96, 12, 12, 160, 4, 2, 1),
+    # image side at the c4 shape (lowered im2col / column-GEMM + col2im paths)
+    (4, 3, 64, 64, 64, 4, 2, 1),
 ]
 
 
@@ -123,6 +125,7 @@ CONVT_CASES = [
     (4, 128, 16, 16, 64, 4, 2, 1),
     (3, 256, 4, 4, 128, 4, 2, 1),
     (3, 64, 7, 7, 32, 4, 2, 1),
+    (4, 64, 32, 32, 3, 4, 2, 1),
 ]
 
 

