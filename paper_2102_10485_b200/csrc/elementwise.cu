@@ -90,14 +90,16 @@ __global__ void bn_stats_finalize_kernel(ChannelMap cm, const float* stat, float
   const int l = blockIdx.y, c = blockIdx.x * 32 + threadIdx.x, j = threadIdx.y;
   __shared__ Moments sm[8][32];
   Moments a{0.0, 0.0, 0.0};
+  const int W = cm.Cp * cm.npack;  // statistic row width
   if (c < cm.Cp) {
-    for (int s = j; s < cm.nslot; s += 8) {
-      const float* e = stat + ((long long)l * cm.nslot + s) * 4 * cm.Cp + c;
-      const double nb = e[3 * cm.Cp];
-      if (nb <= 0.0) continue;
-      const double s1 = e[cm.Cp], s2 = e[2 * cm.Cp];
-      chan_merge(a, nb, (double)e[0] + s1 / nb, fmax(s2 - s1 * s1 / nb, 0.0));
-    }
+    for (int s = j; s < cm.nslot; s += 8)
+      for (int q = 0; q < cm.npack; ++q) {
+        const float* e = stat + ((long long)l * cm.nslot + s) * 4 * W + q * cm.Cp + c;
+        const double nb = e[3 * W];
+        if (nb <= 0.0) continue;
+        const double s1 = e[W], s2 = e[2 * W];
+        chan_merge(a, nb, (double)e[0] + s1 / nb, fmax(s2 - s1 * s1 / nb, 0.0));
+      }
   }
   sm[j][threadIdx.x] = a;
   __syncthreads();
@@ -122,13 +124,15 @@ __global__ void slot_sum_kernel(ChannelMap cm, const float* stat, float* out) {
   const int l = blockIdx.y, c = blockIdx.x * 32 + threadIdx.x, j = threadIdx.y;
   __shared__ float sm[3][8][33];
   float t[3] = {0.f, 0.f, 0.f};
+  const int W = cm.Cp * cm.npack;
   if (c < cm.Cp)
-    for (int s = j; s < cm.nslot; s += 8) {
-      const float* e = stat + ((long long)l * cm.nslot + s) * 4 * cm.Cp + c;
-      t[0] += e[0];
-      t[1] += e[cm.Cp];
-      t[2] += e[2 * cm.Cp];
-    }
+    for (int s = j; s < cm.nslot; s += 8)
+      for (int q = 0; q < cm.npack; ++q) {
+        const float* e = stat + ((long long)l * cm.nslot + s) * 4 * W + q * cm.Cp + c;
+        t[0] += e[0];
+        t[1] += e[W];
+        t[2] += e[2 * W];
+      }
   for (int k = 0; k < 3; ++k) sm[k][j][threadIdx.x] = t[k];
   __syncthreads();
   if (j < 3 && c < cm.Cp) {

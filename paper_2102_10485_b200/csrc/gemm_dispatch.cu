@@ -91,11 +91,12 @@ double gemm_timing_read_ms() {
   return total;
 }
 
-int gemm_stat_slots(const GemmArgs& a, int math) {
+int gemm_stat_slots(const GemmArgs& a, int math, int* npack) {
+  if (npack) *npack = 1;
   if (math == MATH_FP32_SIMT) return 0;
   if (lowered_enabled(a) && gemm_lowered_supported(a)) return gemm_lowered_stat_slots(a);
   if (gemm_thin_supported(a)) return 0;
-  return gemm_pair_stat_slots(a);
+  return gemm_pair_stat_slots(a, npack);
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {

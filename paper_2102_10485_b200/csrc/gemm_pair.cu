@@ -47,6 +47,7 @@ constexpr int NDRAIN = 8;
 constexpr int NT = (4 + NDRAIN) * 32;
 constexpr int W_MMA = 3, W_DRAIN = 4;
 constexpr int SMEM_BUDGET = 200 * 1024;
+constexpr int KIND_DGP = 3;  // phase-packed stride-2 DGRAD (k = 4, s = 2, p = 1), engine-internal
 #ifndef PG_PAIR_SL
 #define PG_PAIR_SL 0
 #endif
@@ -66,6 +67,8 @@ struct PairPlan {
   float slope;
   int accumulate, c_valid, c_pad;
   int stat_mode, nslot;
+  int CGn;  // output channels (stat_mu stride; = N except phase-packed DGRAD)
+  int stage_tx;  // TMA bytes per stage (A box rows may be < 128: the rest of the tile is never read back)
   float* stat;
   const float* stat_y;
   const float* stat_z;
@@ -110,52 +113,86 @@ PG_DEV float act_t(float x, float slope) {
   return x;
 }
 
+// Where one accumulator row's columns go.  Plain tiles: the row is one output
+// pixel, column n = channel n at offset off0 + n.  Phase-packed DGRAD tiles
+// (KIND_DGP): the row is a base position (b, i0, j0) of the stride-2 grid and
+// column n = (phase, channel) with phase = n / CG, i.e. output pixel
+// (2 i0 - 1 + ry, 2 j0 - 1 + rx) -- each 2x2 output block reads the same 2x2
+// small-map neighbourhood, so all four phases share one A operand.
+struct RowPix {
+  long long off0;  // plain: per-label offset of channel 0 (-1: padding row)
+  int b, i0, j0;   // packed: base position (b < 0: padding row)
+  int packed, CG, GH, GW;
+  PG_DEV int chan(int n) const { return packed ? n % CG : n; }
+  // per-label offset of column n's element, -1 when it does not exist
+  PG_DEV long long addr(int n) const {
+    if (!packed) return off0 < 0 ? -1 : off0 + n;
+    if (b < 0) return -1;
+    const int ph = n / CG;
+    const int y = 2 * i0 - 1 + (ph >> 1), x = 2 * j0 - 1 + (ph & 1);
+    if (y < 0 || y >= GH || x < 0 || x >= GW) return -1;
+    return (((long long)b * GH + y) * GW + x) * CG + n % CG;
+  }
+};
+
 // bias, padding columns (written 0) and activation of one output row
 template <int ACT, int BH>
-PG_DEV void epi_store(const float (&acc)[BH], float* crow, int nb, const float* bias, const PairPlan& P) {
+PG_DEV void epi_store(const float (&acc)[BH], const RowPix& rp, float* out, int nb, const float* bias,
+                      const PairPlan& P) {
   const bool padded = P.c_valid != P.c_pad;
 #pragma unroll
   for (int c4 = 0; c4 < BH; c4 += 4) {
     const int n = nb + c4;
     if (n >= P.N) break;
+    const long long a = rp.addr(n);
+    if (a < 0) continue;
+    const int ch = rp.chan(n);
     float o[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       float x = acc[c4 + u];
-      if (bias) x += bias[n + u];
+      if (bias) x += bias[ch + u];
       x = act_t<ACT>(x, P.slope);
-      if (padded && (n + u) % P.c_pad >= P.c_valid) x = 0.f;
+      if (padded && (ch + u) % P.c_pad >= P.c_valid) x = 0.f;
       o[u] = x;
     }
-    *reinterpret_cast<float4*>(crow + n) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(out + a) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
 // output row + per-channel statistics over the warp's 32 rows (StatMode);
-// warp-uniform: every lane runs it, padding rows contribute nothing
+// warp-uniform: every lane runs it, padding rows / missing phase pixels
+// contribute nothing.  Statistics are per GEMM column (packed tiles: per
+// (phase, channel), folded by the finalize kernels).
 template <int MODE, int BH>
-PG_DEV void epi_stats(const float (&acc)[BH], bool valid, long long lo_off, int nb, const float* bias, float* st,
+PG_DEV void epi_stats(const float (&acc)[BH], const RowPix& rp, float* out, int nb, const float* bias, float* st,
                       int label, int lane, const PairPlan& P) {
   const bool padded = P.c_valid != P.c_pad;
-  const float rows = (float)__popc(__ballot_sync(0xffffffffu, valid));
   const int col = red8_col(lane);
 #pragma unroll
   for (int c8 = 0; c8 < BH; c8 += 8) {
     const int n0 = nb + c8;
     if (n0 >= P.N) break;
+    const long long a = rp.addr(n0);
+    const bool valid = a >= 0;
+    const long long lo_off = valid ? a : 0;  // per-label offset of this thread's 8 elements
+    const int ch = rp.chan(n0);
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    const float rows = (float)__popc(vmask);
+    const int src = vmask ? __ffs(vmask) - 1 : 0;  // shift from a real row (never a stale one)
     float v[8], w[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       float x = acc[c8 + u];
-      if (bias) x += bias[n0 + u];
-      if (padded && (n0 + u) % P.c_pad >= P.c_valid) x = 0.f;
+      if (bias) x += bias[ch + u];
+      if (padded && (ch + u) % P.c_pad >= P.c_valid) x = 0.f;
       v[u] = x;
     }
     if (MODE != STAT_FWD) {
 #pragma unroll
       for (int u4 = 0; u4 < 8; u4 += 4) {
         float4 y4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) y4 = __ldg(reinterpret_cast<const float4*>(P.stat_y + lo_off + n0 + u4));
+        if (valid) y4 = __ldg(reinterpret_cast<const float4*>(P.stat_y + (long long)label * P.out_ls + lo_off + u4));
         v[u4] = act_bwd_rl(P.stat_act, v[u4], y4.x, P.stat_slope);
         v[u4 + 1] = act_bwd_rl(P.stat_act, v[u4 + 1], y4.y, P.stat_slope);
         v[u4 + 2] = act_bwd_rl(P.stat_act, v[u4 + 2], y4.z, P.stat_slope);
@@ -163,7 +200,7 @@ PG_DEV void epi_stats(const float (&acc)[BH], bool valid, long long lo_off, int 
       }
     }
     if (valid) {
-      float* crow = P.out + lo_off + n0;
+      float* crow = out + lo_off;
       *reinterpret_cast<float4*>(crow) = make_float4(v[0], v[1], v[2], v[3]);
       *reinterpret_cast<float4*>(crow + 4) = make_float4(v[4], v[5], v[6], v[7]);
     }
@@ -173,8 +210,8 @@ PG_DEV void epi_stats(const float (&acc)[BH], bool valid, long long lo_off, int 
       // with Chan's formula by bn_stats_finalize
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float sh = __shfl_sync(0xffffffffu, v[u], 0);
-        if (lane == 0) s8[u] = sh;
+        const float sh = __shfl_sync(0xffffffffu, v[u], src);
+        if (lane == src) s8[u] = sh;
         v[u] = valid ? v[u] - sh : 0.f;
         w[u] = v[u] * v[u];
       }
@@ -186,12 +223,12 @@ PG_DEV void epi_stats(const float (&acc)[BH], bool valid, long long lo_off, int 
         s8[3 * P.N + col] = rows;
       }
     } else if (MODE == STAT_BWD_BN) {
-      const float* mu = P.stat_mu + (long long)label * P.N + n0;
+      const float* mu = P.stat_mu + (long long)label * P.CGn + ch;
       float t[8];
 #pragma unroll
       for (int u4 = 0; u4 < 8; u4 += 4) {
         float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) z4 = __ldg(reinterpret_cast<const float4*>(P.stat_z + lo_off + n0 + u4));
+        if (valid) z4 = __ldg(reinterpret_cast<const float4*>(P.stat_z + (long long)label * P.out_ls + lo_off + u4));
         w[u4] = valid ? z4.x - mu[u4] : 0.f;
         w[u4 + 1] = valid ? z4.y - mu[u4 + 1] : 0.f;
         w[u4 + 2] = valid ? z4.z - mu[u4 + 2] : 0.f;
@@ -252,6 +289,152 @@ PG_DEV void pair_tile_decode(const PairPlan& P, int t, int& label, int& phase, i
 // TMEM accumulation buffers (segments in flight between the MMA and the drain)
 __host__ __device__ constexpr int seg_bufs(int bn) { return 512 / bn > 4 ? 4 : 512 / bn; }
 
+// TMA boxes of k-block kb for this CTA: its 128 A rows and its B half
+template <int KIND, int BH>
+PG_DEV void pair_issue(const CUtensorMap& tmA, const CUtensorMap& tmB, const PairPlan& P, uint32_t a_dst,
+                       uint32_t b_dst, uint64_t* bar, int kb, int label, int mtp, uint32_t rank, int n0, int b0,
+                       int i0, int j0, const DgPhase& d) {
+  const ConvGeo& g = P.g;
+  if (KIND == GEMM_FPROP) {
+    const int tap = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
+    const int ki = tap / g.k, kj = tap % g.k;
+    tma_load_5d(a_dst, &tmA, bar, c0, j0 * g.s - g.p + kj, i0 * g.s - g.p + ki, b0, label);
+    tma_load_3d(b_dst, &tmB, bar, kb * BKT, n0, label);
+  } else if (KIND == KIND_DGP) {
+    // k-block = (neighbour (di, dj) of the 2x2 small-map block, 32 input channels)
+    const int nbr = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
+    const int di = nbr >> 1, dj = nbr & 1;
+    tma_load_5d(a_dst, &tmA, bar, c0, j0 - dj, i0 - di, b0, label);
+#pragma unroll
+    for (int q = 0; q < BH / 32; ++q) {
+      const int n = n0 + 32 * q, ph = n / g.CG;
+      const int ki = (ph >> 1) + 2 * di, kj = (ph & 1) + 2 * dj;
+      tma_load_4d(b_dst + q * (BKT * 128), &tmB, bar, n % g.CG, ki * g.k + kj, c0, label);
+    }
+  } else if (KIND == GEMM_DGRAD) {
+    const int tp = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
+    const int ty = tp / d.ntx, tx = tp % d.ntx;
+    const int ki = d.ry + ty * g.s, kj = d.rx + tx * g.s;
+    const int offy = (d.y0 + g.p - d.ry) / g.s - ty;
+    const int offx = (d.x0 + g.p - d.rx) / g.s - tx;
+    tma_load_5d(a_dst, &tmA, bar, c0, j0 + offx, i0 + offy, b0, label);
+#pragma unroll
+    for (int q = 0; q < BH / 32; ++q)
+      tma_load_4d(b_dst + q * (BKT * 128), &tmB, bar, n0 + 32 * q, ki * g.k + kj, c0, label);
+  } else {
+    int kb0, ki0, kj0;
+    box_origin(P.box, kb, kb0, ki0, kj0);
+    const int m0 = mtp * (2 * BM) + (int)rank * BM;
+#pragma unroll
+    for (int q = 0; q < BM / 32; ++q) {
+      const int m = m0 + 32 * q;
+      const int tap = m / g.CG, cg0 = m % g.CG;
+      const int ki = tap / g.k, kj = tap % g.k;
+      tma_load_5d(a_dst + q * (BKT * 128), &tmA, bar, cg0, kj0 * g.s - g.p + kj,
+          ki0 * g.s - g.p + ki, kb0, label);
+    }
+#pragma unroll
+    for (int q = 0; q < BH / 32; ++q)
+      tma_load_5d(b_dst + q * (BKT * 128), &tmB, bar, n0 + 32 * q, kj0, ki0, kb0, label);
+  }
+}
+
+// drain + epilogue role: drain warp dw (0..7) reads TMEM lane quarter dw%4 and
+// accumulator column half dw/4 of every segment into fp32 registers, then
+// writes the tile (epi_store / epi_stats)
+template <int KIND, int BN, bool STATS, int NB>
+PG_DEV void pair_drain_role(const PairPlan& P, uint32_t tmem, uint64_t* seg_full, uint64_t* seg_empty, int dw,
+                            int lane, uint32_t rank, int cl, int ncl, int ntiles) {
+  constexpr int BH = BN / 2;
+  const ConvGeo& g = P.g;
+  const int warp = dw + W_DRAIN;
+    const int q = warp & 3;               // TMEM lane quarter
+    const int half = (warp - W_DRAIN) >> 2;  // accumulator column half
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const uint32_t seg_empty_leader = mapa_shared(smem_u32(seg_empty), 0);
+    uint32_t sc = 0;
+    for (int t = cl; t < ntiles; t += ncl) {
+      int label, phase, mtp, nt;
+      pair_tile_decode(P, t, label, phase, mtp, nt);
+      const int row = q * 32 + lane;
+      const int nb = nt * BN + half * BH;  // first output column of this thread
+      float acc[BH];
+#pragma unroll
+      for (int i = 0; i < BH; ++i) acc[i] = 0.f;
+      for (int k_seg = 0; k_seg < P.nk; k_seg += P.kseg, ++sc) {
+        const uint32_t buf = sc % NB;
+        mbar_wait_cluster(seg_full + buf, (sc / NB) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < BH / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_base + buf * BN + half * BH + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[c * 32 + i] += __uint_as_float(r[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(seg_empty_leader + buf * 8);
+      }
+      RowPix rp{-1, -1, 0, 0, KIND == KIND_DGP, g.CG, g.GH, g.GW};
+      if (KIND != GEMM_WGRAD) {
+        int b0, i0, j0;
+        box_origin(P.box, 2 * mtp + (int)rank, b0, i0, j0);
+        const bool in_box = row < P.box.TB * P.box.TH * P.box.TW;  // rows past a short box hold stale data
+        const int b = in_box ? b0 + row / (P.box.TH * P.box.TW) : g.B;
+        const int ii = i0 + (row / P.box.TW) % P.box.TH;
+        const int jj = j0 + row % P.box.TW;
+        rp.i0 = ii;
+        rp.j0 = jj;
+        if (KIND == GEMM_FPROP) {
+          if (b < g.B && ii < g.SH && jj < g.SW) rp.off0 = (((long long)b * g.SH + ii) * g.SW + jj) * g.CS;
+        } else if (KIND == GEMM_DGRAD) {
+          const DgPhase d = dg_phase(g, phase);
+          if (b < g.B && ii < d.ny && jj < d.nx)
+            rp.off0 = (((long long)b * g.GH + d.y0 + ii * g.s) * g.GW + d.x0 + jj * g.s) * g.CG;
+        } else {
+          if (b < g.B && ii <= g.GH / 2 && jj <= g.GW / 2) rp.b = b;
+        }
+      }
+      if (KIND == GEMM_WGRAD) {
+        const int m = mtp * (2 * BM) + (int)rank * BM + row;
+        if (m < P.mrows) {
+          float* base = P.out + (long long)label * P.out_ls + m;
+#pragma unroll
+          for (int c = 0; c < BH; ++c) {
+            const int n = nb + c;
+            if (n < P.N) {
+              float* dst = base + (long long)n * P.mrows;
+              *dst = P.accumulate ? *dst + acc[c] : acc[c];
+            }
+          }
+        }
+      } else {
+        const float* bias = P.bias ? P.bias + (long long)label * P.bias_ls : nullptr;
+        float* out = P.out + (long long)label * P.out_ls;
+        if (!STATS) {
+          // one specialised copy per activation: the executed epilogue stays
+          // small (the kernel is instruction-cache sensitive)
+          switch (P.act) {
+            case ACT_RELU: epi_store<ACT_RELU, BH>(acc, rp, out, nb, bias, P); break;
+            case ACT_LRELU: epi_store<ACT_LRELU, BH>(acc, rp, out, nb, bias, P); break;
+            case ACT_TANH: epi_store<ACT_TANH, BH>(acc, rp, out, nb, bias, P); break;
+            case ACT_SIGMOID: epi_store<ACT_SIGMOID, BH>(acc, rp, out, nb, bias, P); break;
+            default: epi_store<ACT_NONE, BH>(acc, rp, out, nb, bias, P); break;
+          }
+          continue;
+        }
+        float* st = P.stat + ((long long)label * P.nslot + ((phase * P.ntmp + mtp) * 2 + (int)rank) * 4 + q) * 4 * P.N;
+        switch (P.stat_mode) {
+          case STAT_FWD: epi_stats<STAT_FWD, BH>(acc, rp, out, nb, bias, st, label, lane, P); break;
+          case STAT_BWD_BN: epi_stats<STAT_BWD_BN, BH>(acc, rp, out, nb, bias, st, label, lane, P); break;
+          default: epi_stats<STAT_BWD_ACT, BH>(acc, rp, out, nb, bias, st, label, lane, P); break;
+        }
+      }
+    }
+  }
+
 template <int KIND, int BN, int MODE, bool STATS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -264,7 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   constexpr int AB = a_bytes();
   constexpr int BH = BN / 2;  // B columns staged per CTA; also the drain column half
   constexpr bool A_MN = KIND == GEMM_WGRAD;
-  constexpr bool B_MN = KIND != GEMM_FPROP;
+  constexpr bool B_MN = KIND != GEMM_FPROP;  // DGRAD / KIND_DGP weights and WGRAD gradients are N-major
   constexpr int NB = seg_bufs(BN);
   constexpr uint32_t TMEM_COLS = NB * BN;
 
@@ -322,40 +505,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
         for (int kb = 0; kb < P.nk; ++kb, ++it) {
           const int s = it % SH;
           mbar_wait(empty_h + s, ((it / SH) & 1) ^ 1);
-          mbar_expect_tx(full_h + s, SB);
+          mbar_expect_tx(full_h + s, P.stage_tx);
           const uint32_t a_dst = smem_u32(smem + s * SB);
           const uint32_t b_dst = a_dst + AB;
-          if (KIND == GEMM_FPROP) {
-            const int tap = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
-            const int ki = tap / g.k, kj = tap % g.k;
-            tma_load_5d(a_dst, &tmA, full_h + s, c0, j0 * g.s - g.p + kj, i0 * g.s - g.p + ki, b0, label);
-            tma_load_3d(b_dst, &tmB, full_h + s, kb * BKT, n0, label);
-          } else if (KIND == GEMM_DGRAD) {
-            const int tp = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
-            const int ty = tp / d.ntx, tx = tp % d.ntx;
-            const int ki = d.ry + ty * g.s, kj = d.rx + tx * g.s;
-            const int offy = (d.y0 + g.p - d.ry) / g.s - ty;
-            const int offx = (d.x0 + g.p - d.rx) / g.s - tx;
-            tma_load_5d(a_dst, &tmA, full_h + s, c0, j0 + offx, i0 + offy, b0, label);
-#pragma unroll
-            for (int q = 0; q < BH / 32; ++q)
-              tma_load_4d(b_dst + q * (BKT * 128), &tmB, full_h + s, n0 + 32 * q, ki * g.k + kj, c0, label);
-          } else {
-            int kb0, ki0, kj0;
-            box_origin(P.box, kb, kb0, ki0, kj0);
-            const int m0 = mtp * (2 * BM) + (int)rank * BM;
-#pragma unroll
-            for (int q = 0; q < BM / 32; ++q) {
-              const int m = m0 + 32 * q;
-              const int tap = m / g.CG, cg0 = m % g.CG;
-              const int ki = tap / g.k, kj = tap % g.k;
-              tma_load_5d(a_dst + q * (BKT * 128), &tmA, full_h + s, cg0, kj0 * g.s - g.p + kj,
-                          ki0 * g.s - g.p + ki, kb0, label);
-            }
-#pragma unroll
-            for (int q = 0; q < BH / 32; ++q)
-              tma_load_5d(b_dst + q * (BKT * 128), &tmB, full_h + s, n0 + 32 * q, kj0, ki0, kb0, label);
-          }
+          pair_issue<KIND, BH>(tmA, tmB, P, a_dst, b_dst, full_h + s, kb, label, mtp, rank, n0, b0, i0, j0, d);
         }
       }
     }
@@ -436,89 +589,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     }
     __syncwarp();
   } else {
-    // ===================== drain + epilogue (both CTAs) =====================
-    const int q = warp & 3;               // TMEM lane quarter
-    const int half = (warp - W_DRAIN) >> 2;  // accumulator column half
-    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    const uint32_t seg_empty_leader = mapa_shared(smem_u32(seg_empty), 0);
-    uint32_t sc = 0;
-    for (int t = cl; t < ntiles; t += ncl) {
-      int label, phase, mtp, nt;
-      pair_tile_decode(P, t, label, phase, mtp, nt);
-      float acc[BH];
-#pragma unroll
-      for (int i = 0; i < BH; ++i) acc[i] = 0.f;
-      for (int k_seg = 0; k_seg < P.nk; k_seg += P.kseg, ++sc) {
-        const uint32_t buf = sc % NB;
-        mbar_wait_cluster(seg_full + buf, (sc / NB) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < BH / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tmem + lane_base + buf * BN + half * BH + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) acc[c * 32 + i] += __uint_as_float(r[i]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote(seg_empty_leader + buf * 8);
-      }
-      const int row = q * 32 + lane;
-      const int nb = nt * BN + half * BH;  // first output column of this thread
-      if (KIND == GEMM_WGRAD) {
-        const int m = mtp * (2 * BM) + (int)rank * BM + row;
-        if (m < P.mrows) {
-          float* base = P.out + (long long)label * P.out_ls + m;
-#pragma unroll
-          for (int c = 0; c < BH; ++c) {
-            const int n = nb + c;
-            if (n < P.N) {
-              float* dst = base + (long long)n * P.mrows;
-              *dst = P.accumulate ? *dst + acc[c] : acc[c];
-            }
-          }
-        }
-      } else {
-        int b0, i0, j0;
-        box_origin(P.box, 2 * mtp + (int)rank, b0, i0, j0);
-        const int b = b0 + row / (P.box.TH * P.box.TW);
-        const int ii = i0 + (row / P.box.TW) % P.box.TH;
-        const int jj = j0 + row % P.box.TW;
-        long long off = -1;  // this row's offset in the output map (per label), -1 = padding row
-        if (KIND == GEMM_FPROP) {
-          if (b < g.B && ii < g.SH && jj < g.SW) off = (((long long)b * g.SH + ii) * g.SW + jj) * g.CS;
-        } else {
-          const DgPhase d = dg_phase(g, phase);
-          if (b < g.B && ii < d.ny && jj < d.nx)
-            off = (((long long)b * g.GH + d.y0 + ii * g.s) * g.GW + d.x0 + jj * g.s) * g.CG;
-        }
-        const bool valid = off >= 0;
-        const float* bias = P.bias ? P.bias + (long long)label * P.bias_ls : nullptr;
-        if (!STATS) {
-          if (valid) {
-            float* crow = P.out + (long long)label * P.out_ls + off;
-            // one specialised copy per activation: the executed epilogue stays
-            // small (the kernel is instruction-cache sensitive)
-            switch (P.act) {
-              case ACT_RELU: epi_store<ACT_RELU, BH>(acc, crow, nb, bias, P); break;
-              case ACT_LRELU: epi_store<ACT_LRELU, BH>(acc, crow, nb, bias, P); break;
-              case ACT_TANH: epi_store<ACT_TANH, BH>(acc, crow, nb, bias, P); break;
-              case ACT_SIGMOID: epi_store<ACT_SIGMOID, BH>(acc, crow, nb, bias, P); break;
-              default: epi_store<ACT_NONE, BH>(acc, crow, nb, bias, P); break;
-            }
-          }
-          continue;
-        }
-        const long long lo_off = (long long)label * P.out_ls + (valid ? off : 0);
-        float* st = P.stat + ((long long)label * P.nslot + ((phase * P.ntmp + mtp) * 2 + (int)rank) * 4 + q) * 4 * P.N;
-        switch (P.stat_mode) {
-          case STAT_FWD: epi_stats<STAT_FWD, BH>(acc, valid, lo_off, nb, bias, st, label, lane, P); break;
-          case STAT_BWD_BN: epi_stats<STAT_BWD_BN, BH>(acc, valid, lo_off, nb, bias, st, label, lane, P); break;
-          default: epi_stats<STAT_BWD_ACT, BH>(acc, valid, lo_off, nb, bias, st, label, lane, P); break;
-        }
-      }
-    }
+    pair_drain_role<KIND, BN, STATS, NB>(P, tmem, seg_full, seg_empty, warp - W_DRAIN, lane, rank, cl, ncl, ntiles);
   }
   tc_fence_before();
   __syncthreads();
@@ -526,6 +597,201 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   if (warp == W_MMA) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, TMEM_COLS);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// A-in-TMEM variant for the narrow tiles (BN <= 128, TF32X3, FPROP / DGRAD).
+// At BN = 64 the single-CTA-equivalent MMA rate needs ~300 B/clk of shared
+// memory in the SS form (the tensor core re-reads A for all three products of
+// the split) against 128 B/clk available; here the split warps read each A row
+// once, write its hi and lo parts to tensor memory (tcgen05.st), and the MMA
+// reads A from TMEM ("TS" form), B (hi from the stage, lo from a small ring)
+// from shared memory.
+//   warps 0-3  split: lane quarter q = warp, thread = A row; B half lo -> smem
+//   warps 4-11 drain + epilogue (as pair_drain_role)
+//   warp 12    TMA producer;  warp 13  TMEM allocation + MMA issuer (leader)
+// TMEM: accumulator buffers in columns [0, 256), A stages (hi 32 + lo 32
+// columns each) in [256, 512).
+constexpr int ATM_NT = 14 * 32;
+constexpr int ATM_SA = 4;
+constexpr int ATM_ACOL = 256;
+__host__ __device__ constexpr int atm_bufs(int bn) { return 256 / bn; }
+__host__ __device__ constexpr int atm_lo_bytes(int bn) { return (bn / 2) * BKT * 4; }
+__host__ __device__ constexpr int atm_hi_stages(int bn) {
+  return (SMEM_BUDGET - ATM_SA * atm_lo_bytes(bn)) / stage_bytes(bn) > 8
+             ? 8
+             : (SMEM_BUDGET - ATM_SA * atm_lo_bytes(bn)) / stage_bytes(bn);
+}
+__host__ __device__ constexpr int atm_smem(int bn) {
+  return atm_hi_stages(bn) * stage_bytes(bn) + ATM_SA * atm_lo_bytes(bn) + 1024 + 1024;
+}
+
+template <int KIND, int BN, bool STATS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
+    gemm_pair_atm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const PairPlan P) {
+  static_assert(BN <= 128 && KIND != GEMM_WGRAD, "A-in-TMEM tiles: K-major A, BN <= 128");
+  constexpr int SH = atm_hi_stages(BN);
+  constexpr int SB = stage_bytes(BN);
+  constexpr int AB = a_bytes();
+  constexpr int BH = BN / 2;
+  constexpr int LB = atm_lo_bytes(BN);
+  constexpr bool B_MN = KIND != GEMM_FPROP;
+  constexpr int NB = atm_bufs(BN);
+  constexpr int W_TMA = 12, W_MMAI = 13;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* lo_base = smem + SH * SB;
+  uint64_t* full_h = reinterpret_cast<uint64_t*>(lo_base + ATM_SA * LB);
+  uint64_t* empty_h = full_h + SH;
+  uint64_t* ready = empty_h + SH;
+  uint64_t* empty_l = ready + ATM_SA;
+  uint64_t* seg_full = empty_l + ATM_SA;
+  uint64_t* seg_empty = seg_full + NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(seg_empty + NB);
+
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int ntiles = P.ntn * P.ntmp * P.nz;
+
+  if (tid == 0) {
+    for (int s = 0; s < SH; ++s) {
+      mbar_init(full_h + s, 1);
+      mbar_init(empty_h + s, 1);
+    }
+    for (int s = 0; s < ATM_SA; ++s) {
+      mbar_init(ready + s, 2 * 4);
+      mbar_init(empty_l + s, 1);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(seg_full + b, 1);
+      mbar_init(seg_empty + b, 2 * NDRAIN);
+    }
+    fence_barrier_init();
+  }
+  if (warp == W_MMAI) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ===================== split: A rows -> TMEM (hi, lo); B half lo -> smem =====================
+    const int r = warp * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t ready_leader = mapa_shared(smem_u32(ready), 0);
+    uint32_t it = 0;
+    for (int t = cl; t < ntiles; t += ncl) {
+      for (int kb = 0; kb < P.nk; ++kb, ++it) {
+        const int s = it % SH, j = it % ATM_SA;
+        mbar_wait(full_h + s, (it / SH) & 1);
+        mbar_wait(empty_l + j, ((it / ATM_SA) & 1) ^ 1);
+        // row r of the K-major SW128 A tile: 16-byte chunk c sits at c ^ (r & 7)
+        const uint8_t* arow = smem + s * SB + r * 128;
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = *reinterpret_cast<const float4*>(arow + ((c ^ (r & 7)) << 4));
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            hi[4 * c + u] = __float_as_uint(e[u]);
+            lo[4 * c + u] = __float_as_uint(e[u] - tf32_trunc(e[u]));
+          }
+        }
+        const uint32_t ta = tmem + lane_off + ATM_ACOL + j * 64;
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        const float4* bsrc = reinterpret_cast<const float4*>(smem + s * SB + AB);
+        float4* bdst = reinterpret_cast<float4*>(lo_base + j * LB);
+#pragma unroll
+        for (int e = tid; e < LB / 16; e += 128) {
+          const float4 v = bsrc[e];
+          bdst[e] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                                v.w - tf32_trunc(v.w));
+        }
+        tmem_st_wait();
+        fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(ready_leader + j * 8);
+      }
+    }
+  } else if (warp < 4 + NDRAIN) {
+    pair_drain_role<KIND, BN, STATS, NB>(P, tmem, seg_full, seg_empty, warp - W_DRAIN, lane, rank, cl, ncl, ntiles);
+  } else if (warp == W_TMA) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      uint32_t it = 0;
+      for (int t = cl; t < ntiles; t += ncl) {
+        int label, phase, mtp, nt;
+        pair_tile_decode(P, t, label, phase, mtp, nt);
+        const int n0 = nt * BN + (int)rank * BH;
+        int b0 = 0, i0 = 0, j0 = 0;
+        box_origin(P.box, 2 * mtp + (int)rank, b0, i0, j0);
+        DgPhase d{};
+        if (KIND == GEMM_DGRAD) d = dg_phase(P.g, phase);
+        for (int kb = 0; kb < P.nk; ++kb, ++it) {
+          const int s = it % SH;
+          mbar_wait(empty_h + s, ((it / SH) & 1) ^ 1);
+          mbar_expect_tx(full_h + s, P.stage_tx);
+          const uint32_t a_dst = smem_u32(smem + s * SB);
+          pair_issue<KIND, BH>(tmA, tmB, P, a_dst, a_dst + AB, full_h + s, kb, label, mtp, rank, n0, b0, i0, j0, d);
+        }
+      }
+    }
+  } else {
+    // ===================== MMA issuer (leader CTA only): A from TMEM =====================
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = make_idesc(2 * BM, BN, false, B_MN);
+      constexpr uint32_t b_lbo = B_MN ? 4096u : 16u, b_sbo = B_MN ? 512u : 1024u, b_step = B_MN ? 1024u : 32u;
+      constexpr uint32_t b_lay = B_MN ? UMMA_SW128_BASE32B : UMMA_SW128;
+      uint32_t it = 0, sc = 0;
+      for (int t = cl; t < ntiles; t += ncl) {
+        for (int k_seg = 0; k_seg < P.nk; k_seg += P.kseg, ++sc) {
+          const uint32_t buf = sc % NB;
+          mbar_wait_cluster(seg_empty + buf, ((sc / NB) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t dacc = tmem + buf * BN;
+          const int k_end = min(P.nk, k_seg + P.kseg);
+          for (int kb = k_seg; kb < k_end; ++kb, ++it) {
+            const int s = it % SH, j = it % ATM_SA;
+            mbar_wait_cluster(ready + j, (it / ATM_SA) & 1);
+            tc_fence_after();
+            const uint32_t a_t = tmem + ATM_ACOL + j * 64;
+            const uint32_t b_hi = smem_u32(smem + s * SB) + AB;
+            const uint32_t b_lo = smem_u32(lo_base + j * LB);
+#pragma unroll
+            for (int kk = 0; kk < BKT / 8; ++kk) {
+              const uint64_t bh = make_desc(b_hi + kk * b_step, b_lbo, b_sbo, b_lay);
+              const uint64_t bl = make_desc(b_lo + kk * b_step, b_lbo, b_sbo, b_lay);
+              const uint32_t acc = (kb != k_seg || kk) ? 1u : 0u;
+              mma_tf32_pair_ts(dacc, a_t + 32 + kk * 8, bh, idesc, acc);  // small terms first
+              mma_tf32_pair_ts(dacc, a_t + kk * 8, bl, idesc, 1u);
+              mma_tf32_pair_ts(dacc, a_t + kk * 8, bh, idesc, 1u);
+            }
+            mma_commit_pair(empty_h + s, 3);
+            mma_commit_pair(empty_l + j, 3);
+          }
+          mma_commit_pair(seg_full + buf, 3);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == W_MMAI) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
   }
 }
 
@@ -546,11 +812,41 @@ cudaError_t launch_pair_st(const CUtensorMap& ta, const CUtensorMap& tb, const P
   return launched();
 }
 
+template <int KIND, int BN, bool STATS>
+cudaError_t launch_pair_atm(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, int grid,
+                            cudaStream_t st) {
+  constexpr int smem = atm_smem(BN);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_pair_atm_kernel<KIND, BN, STATS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  gemm_pair_atm_kernel<KIND, BN, STATS><<<grid, ATM_NT, smem, st>>>(ta, tb, P);
+  return launched();
+}
+
+// A-in-TMEM tiles: correct, but measured no faster than the SS form in the
+// full step (82.6 vs 82.5 ms; the narrow tiles are L2-feed bound), so opt-in
+bool atm_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PG_ATM");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 template <int KIND, int BN, int MODE>
 cudaError_t launch_pair_bn(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, cudaStream_t st) {
   const int tiles = P.ntn * P.ntmp * P.nz;
   if (tiles == 0 || P.nk == 0) return cudaSuccess;
   const int pairs = std::min(tiles, sm_count_tma() / 2);
+  if constexpr (KIND != GEMM_WGRAD && BN <= 128 && MODE == MATH_TF32X3) {
+    if (atm_enabled())
+      return P.stat_mode != STAT_NONE ? launch_pair_atm<KIND, BN, true>(ta, tb, P, 2 * pairs, st)
+                                      : launch_pair_atm<KIND, BN, false>(ta, tb, P, 2 * pairs, st);
+  }
   if (KIND != GEMM_WGRAD && P.stat_mode != STAT_NONE)
     return launch_pair_st<KIND, BN, MODE, KIND != GEMM_WGRAD>(ta, tb, P, 2 * pairs, st);
   return launch_pair_st<KIND, BN, MODE, false>(ta, tb, P, 2 * pairs, st);
@@ -565,6 +861,43 @@ cudaError_t launch_pair_kind(const CUtensorMap& ta, const CUtensorMap& tb, const
 }
 
 int pair_bn(int n) { return n >= 256 ? 256 : n >= 128 ? 128 : 64; }
+
+// Base grid of the phase-packed DGRAD is (H/2 + 1) x (W/2 + 1) (17 x 17 for a
+// 32 x 32 output): a power-of-two box would waste half the rows, so the box
+// is W wide (whole rows) and at most 128 rows deep, picking the TH x TB split
+// with the least padding; rows past the box are never stored.
+SpatialBox packed_box(int B, int H, int W) {
+  if ((W & (W - 1)) == 0 || W > BM) return spatial_box(B, H, W, BM);
+  SpatialBox best{};
+  double best_util = -1.0;
+  for (int th = 1; th * W <= BM; ++th) {
+    SpatialBox b;
+    b.TW = W;
+    b.TH = std::min(th, H);
+    b.TB = BM / (b.TW * b.TH);
+    b.nx = 1;
+    b.ny = (H + b.TH - 1) / b.TH;
+    b.nb = (B + b.TB - 1) / b.TB;
+    const double util = (double)B * H * W / ((double)b.nb * b.ny * BM);
+    if (util > best_util) {
+      best_util = util;
+      best = b;
+    }
+  }
+  return best;
+}
+
+// phase-packed DGRAD (KIND_DGP): k4 s2 p1 with 4 CG <= 256, where the per-phase
+// form would run BN = 64 tiles re-reading the small map 16 times
+bool dgrad_packed(const GemmArgs& a) {
+  static const bool disabled = [] {
+    const char* e = std::getenv("PG_NO_DGP");
+    return e && std::atoi(e) != 0;
+  }();
+  const ConvGeo& g = a.g;
+  return !disabled && a.kind == GEMM_DGRAD && g.k == 4 && g.s == 2 && g.p == 1 && g.GH == 2 * g.SH &&
+         g.GW == 2 * g.SW && g.CG % 32 == 0 && 4 * g.CG <= 256 && g.CS % 32 == 0;
+}
 
 }  // namespace
 
@@ -591,16 +924,22 @@ bool gemm_pair_supported(const GemmArgs& a) {
   }
 }
 
-int gemm_pair_stat_slots(const GemmArgs& a) {
+int gemm_pair_stat_slots(const GemmArgs& a, int* npack) {
   const ConvGeo& g = a.g;
+  if (npack) *npack = 1;
   if (a.kind == GEMM_WGRAD || !gemm_pair_supported(a)) return 0;
   if (a.kind == GEMM_FPROP) {
     const SpatialBox b = spatial_box(g.B, g.SH, g.SW, BM);
     if (g.CS % 8) return 0;
     return (b.nb * b.ny * b.nx + 1) / 2 * 8;
   }
-  const SpatialBox b = spatial_box(g.B, (g.GH + g.s - 1) / g.s, (g.GW + g.s - 1) / g.s, BM);
   if (g.CG % 8) return 0;
+  if (dgrad_packed(a)) {
+    const SpatialBox b = packed_box(g.B, g.GH / 2 + 1, g.GW / 2 + 1);
+    if (npack) *npack = 4;
+    return (b.nb * b.ny * b.nx + 1) / 2 * 8;
+  }
+  const SpatialBox b = spatial_box(g.B, (g.GH + g.s - 1) / g.s, (g.GW + g.s - 1) / g.s, BM);
   return g.s * g.s * ((b.nb * b.ny * b.nx + 1) / 2) * 8;
 }
 
@@ -656,6 +995,23 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
     const long long bs[2] = {K, a.w_ls};
     const int bbox[3] = {BKT, bn / 2, 1};
     ok = ok && make_map(&tb, a.w, 3, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if (dgrad_packed(a)) {
+    P.N = 4 * g.CG;
+    P.kcb = g.CS / BKT;
+    P.nk = 4 * P.kcb;
+    P.phases = 1;
+    P.nz = a.L;
+    P.box = packed_box(g.B, g.GH / 2 + 1, g.GW / 2 + 1);
+    ntm = P.box.nb * P.box.ny * P.box.nx;
+    bn = pair_bn(P.N);
+    const long long ad[5] = {g.CS, g.SW, g.SH, g.B, a.L};
+    const long long as[4] = {g.CS, (long long)g.SW * g.CS, (long long)g.SH * g.SW * g.CS, a.small_ls};
+    const int abox[5] = {BKT, P.box.TW, P.box.TH, P.box.TB, 1};
+    ok = ok && make_map(&ta, a.small, 5, ad, as, abox, one, CU_TENSOR_MAP_SWIZZLE_128B);
+    const long long bd[4] = {g.CG, kk, g.CS, a.L};
+    const long long bs[3] = {g.CG, (long long)kk * g.CG, a.w_ls};
+    const int bbox[4] = {32, 1, BKT, 1};
+    ok = ok && make_map(&tb, a.w, 4, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   } else if (a.kind == GEMM_DGRAD) {
     P.N = g.CG;
     P.kcb = g.CS / BKT;
@@ -696,6 +1052,8 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   P.ntmp = (ntm + 1) / 2;
   P.ntn = (P.N + bn - 1) / bn;
   P.nslot = P.phases * P.ntmp * 8;
+  P.CGn = a.kind == GEMM_FPROP ? g.CS : g.CG;
+  P.stage_tx = (a.kind == GEMM_WGRAD ? BM : P.box.TB * P.box.TH * P.box.TW) * BKT * 4 + (bn / 2) * BKT * 4;
   // profiling aid: PG_FORCE_STATS=1 runs plain FPROP/DGRAD launches with STAT_FWD into a private buffer
   static const bool force_stats = [] {
     const char* e = std::getenv("PG_FORCE_STATS");
@@ -716,6 +1074,9 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   }
   if (P.stat_mode != STAT_NONE && (!P.stat || P.N % 8 || P.act != ACT_NONE)) return cudaErrorInvalidValue;
   const bool x3 = math != MATH_TF32;
+  if (dgrad_packed(a))
+    return x3 ? launch_pair_kind<KIND_DGP, MATH_TF32X3>(ta, tb, P, bn, st)
+              : launch_pair_kind<KIND_DGP, MATH_TF32>(ta, tb, P, bn, st);
   switch (a.kind) {
     case GEMM_FPROP:
       return x3 ? launch_pair_kind<GEMM_FPROP, MATH_TF32X3>(ta, tb, P, bn, st)

@@ -31,11 +31,13 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st);  // 
 bool gemm_pair_supported(const GemmArgs& a);
 cudaError_t launch_gemm_lowered(const GemmArgs& a, int math, cudaStream_t st);  // im2col / col2im + pair engine
 bool gemm_lowered_supported(const GemmArgs& a);
-int gemm_pair_stat_slots(const GemmArgs& a);
+int gemm_pair_stat_slots(const GemmArgs& a, int* npack = nullptr);
 int gemm_lowered_stat_slots(const GemmArgs& a);
 // number of 32-row statistic slots launch_gemm(a, math) writes when a.stat_mode
-// is set (0: the engine chosen for this GEMM cannot fuse statistics)
-int gemm_stat_slots(const GemmArgs& a, int math);
+// is set (0: the engine chosen for this GEMM cannot fuse statistics); *npack =
+// GEMM columns per output channel (4 for phase-packed DGRAD: stat rows are
+// npack * N_out wide, channel c at columns c + q N_out)
+int gemm_stat_slots(const GemmArgs& a, int math, int* npack = nullptr);
 cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st);  // thin.cu
 bool gemm_thin_supported(const GemmArgs& a);
 float* gemm_scratch(size_t floats, cudaStream_t st);  // grow-only workspace for split-K reductions
@@ -55,6 +57,7 @@ struct ChannelMap {
   // partials source: 0 = channel_reduce chunks ([L][chunks][3][Cp]); > 0 = that
   // many GEMM-epilogue statistic slots ([L][slots][4][Cp], see StatMode)
   int nslot = 0;
+  int npack = 1;  // statistic columns per channel (see gemm_stat_slots)
 };
 int reduce_chunks(int R);
 size_t reduce_partial_floats(const ChannelMap& cm);

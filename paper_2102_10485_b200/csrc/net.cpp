@@ -451,13 +451,17 @@ ConvGeo DevNet::geo_for(const Block& b, int B) const {
   return g;
 }
 
-// PG_NO_FUSE bit 1: forward BN statistics, bit 2: backward sums (A/B timing only)
+// Fused epilogue statistics.  bit 1: forward BN moments (default on: saves two
+// reads of every pre-BN map, measured -2 ms/step on c4), bit 2: backward
+// act/BN sums (default off: the y / z reads in the epilogue stall the MMA
+// pipeline more than the separate reduce pass costs, +2.7 ms/step).
+// PG_FUSE overrides the bit set (A/B timing).
 static bool fuse_enabled(int bit) {
-  static const int off = [] {
-    const char* e = std::getenv("PG_NO_FUSE");
-    return e ? std::atoi(e) : 0;
+  static const int on = [] {
+    const char* e = std::getenv("PG_FUSE");
+    return e ? std::atoi(e) : 1;
   }();
-  return !(off & bit);
+  return on & bit;
 }
 
 float* DevNet::stat_buf(size_t floats, cudaStream_t st) {
@@ -509,18 +513,21 @@ void DevNet::forward(Trace& t, int B, bool train, bool update_running, cudaStrea
     GemmArgs a = linear_args(b, B, t.act[i], z, false);
     ChannelMap cm{L_, static_cast<int>(static_cast<long>(B) * b.out.H * b.out.W), static_cast<int>(b.out.Cp),
                   static_cast<int>(b.out.C), static_cast<long long>(B) * b.out.numel()};
-    const int slots = train && fuse_enabled(1) ? gemm_stat_slots(a, math_) : 0;
+    int npack = 1;
+    const int slots = train && fuse_enabled(1) ? gemm_stat_slots(a, math_, &npack) : 0;
     if (slots > 0) {
       // batch statistics fused into the GEMM epilogue (per 32-row slot), merged here
       a.stat_mode = STAT_FWD;
-      a.stat = stat_buf(static_cast<size_t>(L_) * slots * 4 * b.out.Cp, st);
+      a.stat = stat_buf(static_cast<size_t>(L_) * slots * 4 * npack * b.out.Cp, st);
       check_cuda(launch_gemm(a, math_, st), "linear forward");
       cm.nslot = slots;
+      cm.npack = npack;
       check_cuda(launch_bn_stats_finalize(cm, a.stat, t.mean[i].p, t.istd[i].p, running.p + b.off_run, Bf_,
                                           static_cast<float>(b.bn.eps), static_cast<float>(b.bn.momentum),
                                           update_running ? 1 : 0, st),
                  "bn stats finalize");
       cm.nslot = 0;
+      cm.npack = 1;
     } else {
       check_cuda(launch_gemm(a, math_, st), "linear forward");
     }
@@ -548,6 +555,7 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
   const int nb = static_cast<int>(blocks_.size());
   const float* gy = gy_ext;
   int fused = 0;  // > 0: gy already is act_bwd(gy, y) and its channel sums sit in stat_ (that many slots)
+  int fused_pack = 1;
   for (int i = nb - 1; i >= 0; --i) {
     const Block& b = blocks_[static_cast<size_t>(i)];
     const long long out_ls = static_cast<long long>(B) * b.out.numel();
@@ -563,8 +571,10 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
       if (fused) {
         // sums from the producing GEMM's epilogue, pre-reduced over its slots
         cs.nslot = fused;
+        cs.npack = fused_pack;
         check_cuda(launch_slot_sum(cs, stat_.p, partial_.p, st), "bn bwd slot sum");
         cs.nslot = 1;
+        cs.npack = 1;
       } else {
         check_cuda(launch_channel_reduce(cm, RED_BN_BWD, t.pre[i].p, gy, t.act[i + 1], t.mean[i].p, b.act, b.slope,
                                          partial_.p, st),
@@ -587,8 +597,10 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
     if (param_grads && !bias_done && fused && !b.has_bn) {
       ChannelMap cb = cm;
       cb.nslot = fused;
+      cb.npack = fused_pack;
       check_cuda(launch_slot_sum(cb, stat_.p, partial_.p, st), "bias slot sum");
       cb.nslot = 1;
+      cb.npack = 1;
       check_cuda(launch_bias_finalize(cb, partial_.p, dbias, P_, accumulate ? 1 : 0, st), "bias finalize");
       bias_done = true;
     }
@@ -664,10 +676,13 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
         // the previous block's activation backward and BatchNorm / bias sums ride
         // on this GEMM's epilogue when its engine supports it
         const Block& pb = blocks_[static_cast<size_t>(i - 1)];
-        const int slots = (pb.has_bn || pb.act != ACT_NONE) && fuse_enabled(2) ? gemm_stat_slots(a, math_) : 0;
+        int npack = 1;
+        const int slots =
+            (pb.has_bn || pb.act != ACT_NONE) && fuse_enabled(2) ? gemm_stat_slots(a, math_, &npack) : 0;
         if (slots > 0) {
           a.stat_mode = pb.has_bn ? STAT_BWD_BN : STAT_BWD_ACT;
-          a.stat = stat_buf(static_cast<size_t>(L_) * slots * 4 * b.in.Cp, st);
+          a.stat = stat_buf(static_cast<size_t>(L_) * slots * 4 * npack * b.in.Cp, st);
+          fused_pack = npack;
           a.stat_y = t.act[static_cast<size_t>(i)];
           a.stat_z = pb.has_bn ? t.pre[static_cast<size_t>(i - 1)].p : nullptr;
           a.stat_mu = pb.has_bn ? t.mean[static_cast<size_t>(i - 1)].p : nullptr;

@@ -69,6 +69,7 @@ PG_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+PG_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 PG_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // shared-memory matrix descriptor (version 1 = tcgen05); layout 0 = none, 1 = 128B_BASE32B
@@ -163,6 +164,53 @@ PG_DEV void mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint3
       "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// the same with A read from tensor memory (each CTA's 128 rows at column a_tmem)
+PG_DEV void mma_tf32_pair_ts(uint32_t tmem_d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// 32 lanes (the warp's quarter) x 32 columns from registers
+PG_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]),
+      "r"(r[1]),
+      "r"(r[2]),
+      "r"(r[3]),
+      "r"(r[4]),
+      "r"(r[5]),
+      "r"(r[6]),
+      "r"(r[7]),
+      "r"(r[8]),
+      "r"(r[9]),
+      "r"(r[10]),
+      "r"(r[11]),
+      "r"(r[12]),
+      "r"(r[13]),
+      "r"(r[14]),
+      "r"(r[15]),
+      "r"(r[16]),
+      "r"(r[17]),
+      "r"(r[18]),
+      "r"(r[19]),
+      "r"(r[20]),
+      "r"(r[21]),
+      "r"(r[22]),
+      "r"(r[23]),
+      "r"(r[24]),
+      "r"(r[25]),
+      "r"(r[26]),
+      "r"(r[27]),
+      "r"(r[28]),
+      "r"(r[29]),
+      "r"(r[30]),
+      "r"(r[31])
+      : "memory");
+}
+PG_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // arrive on the barrier at this offset in every CTA of `mask` once the pair MMAs issued so far retire
 PG_DEV void mma_commit_pair(uint64_t* bar, uint16_t mask) {
   asm volatile(
