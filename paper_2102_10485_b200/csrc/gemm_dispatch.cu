@@ -25,6 +25,9 @@ bool lowered_enabled(const GemmArgs& a) {
   }();
   return !(off & (a.kind == GEMM_FPROP ? 1 : 2));
 }
+// the 4-channel image-side FPROP runs on the pair engine's direct TMA gather
+// (KIND_F4) ahead of the SIMT thin kernel
+bool image_side_direct(const GemmArgs& a) { return a.kind == GEMM_FPROP && a.g.CG == 4 && gemm_pair_supported(a); }
 }  // namespace
 
 std::string gemm_timing_report() {
@@ -95,6 +98,7 @@ int gemm_stat_slots(const GemmArgs& a, int math, int* npack) {
   if (npack) *npack = 1;
   if (math == MATH_FP32_SIMT) return 0;
   if (lowered_enabled(a) && gemm_lowered_supported(a)) return gemm_lowered_stat_slots(a);
+  if (image_side_direct(a)) return gemm_pair_stat_slots(a, npack);
   if (gemm_thin_supported(a)) return 0;
   return gemm_pair_stat_slots(a, npack);
 }
@@ -109,6 +113,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
   }
   cudaError_t r;
   if (math != MATH_FP32_SIMT && lowered_enabled(a) && gemm_lowered_supported(a)) r = launch_gemm_lowered(a, math, st);
+  else if (math != MATH_FP32_SIMT && image_side_direct(a)) r = launch_gemm_pair(a, math, st);  // 4-channel FPROP
   else if (gemm_thin_supported(a)) r = launch_gemm_thin(a, st);  // image-side / dense-head shapes (fp32 FMA)
   else if (math != MATH_FP32_SIMT && gemm_pair_supported(a)) r = launch_gemm_pair(a, math, st);  // big conv GEMMs
   else if (math != MATH_FP32_SIMT && gemm_tma_supported(a)) r = launch_gemm_tma(a, math, st);  // conv GEMMs

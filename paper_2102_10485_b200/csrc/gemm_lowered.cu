@@ -120,6 +120,7 @@ bool gemm_lowered_supported(const GemmArgs& a) {
   const int kk = g.k * g.k;
   if (g.k == 1 || kk * 4 < 64 || (kk * 4) % 32) return false;
   if (a.kind == GEMM_FPROP && g.CG == 4 && g.CS >= 64 && g.CS % 32 == 0 && a.big_ls % 4 == 0) {
+    if (gemm_pair_supported(a)) return false;  // direct 4-channel TMA gather (gemm_pair.cu KIND_F4)
     GemmArgs p = fprop_1x1(a, g.B, g.SH, g.SW, kk * 4, g.CS);
     p.big = p.w = p.out = reinterpret_cast<float*>(256);
     return gemm_pair_supported(p);

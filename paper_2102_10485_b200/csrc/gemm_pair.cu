@@ -48,6 +48,7 @@ constexpr int NT = (4 + NDRAIN) * 32;
 constexpr int W_MMA = 3, W_DRAIN = 4;
 constexpr int SMEM_BUDGET = 200 * 1024;
 constexpr int KIND_DGP = 3;  // phase-packed stride-2 DGRAD (k = 4, s = 2, p = 1), engine-internal
+constexpr int KIND_F4 = 4;   // FPROP from a 4-channel (padded RGB) map: a k-block = 8 taps x 4 channels
 #ifndef PG_PAIR_SL
 #define PG_PAIR_SL 0
 #endif
@@ -295,7 +296,18 @@ PG_DEV void pair_issue(const CUtensorMap& tmA, const CUtensorMap& tmB, const Pai
                        uint32_t b_dst, uint64_t* bar, int kb, int label, int mtp, uint32_t rank, int n0, int b0,
                        int i0, int j0, const DgPhase& d) {
   const ConvGeo& g = P.g;
-  if (KIND == GEMM_FPROP) {
+  if (KIND == KIND_F4) {
+    // eight 128-row x 16-byte boxes (one per tap) side by side along K: the
+    // no-swizzle K-major layout (core matrix = 8 rows x 4 fp32 = 128 B, +128 B
+    // per 8 rows along M, +2048 B per tap along K)
+#pragma unroll
+    for (int t = 0; t < BKT / 4; ++t) {
+      const int tap = kb * (BKT / 4) + t;
+      const int ki = tap / g.k, kj = tap % g.k;
+      tma_load_5d(a_dst + t * (BM * 16), &tmA, bar, 0, j0 * g.s - g.p + kj, i0 * g.s - g.p + ki, b0, label);
+    }
+    tma_load_3d(b_dst, &tmB, bar, kb * BKT, n0, label);
+  } else if (KIND == GEMM_FPROP) {
     const int tap = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
     const int ki = tap / g.k, kj = tap % g.k;
     tma_load_5d(a_dst, &tmA, bar, c0, j0 * g.s - g.p + kj, i0 * g.s - g.p + ki, b0, label);
@@ -387,7 +399,7 @@ PG_DEV void pair_drain_role(const PairPlan& P, uint32_t tmem, uint64_t* seg_full
         const int jj = j0 + row % P.box.TW;
         rp.i0 = ii;
         rp.j0 = jj;
-        if (KIND == GEMM_FPROP) {
+        if (KIND == GEMM_FPROP || KIND == KIND_F4) {
           if (b < g.B && ii < g.SH && jj < g.SW) rp.off0 = (((long long)b * g.SH + ii) * g.SW + jj) * g.CS;
         } else if (KIND == GEMM_DGRAD) {
           const DgPhase d = dg_phase(g, phase);
@@ -447,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   constexpr int AB = a_bytes();
   constexpr int BH = BN / 2;  // B columns staged per CTA; also the drain column half
   constexpr bool A_MN = KIND == GEMM_WGRAD;
-  constexpr bool B_MN = KIND != GEMM_FPROP;  // DGRAD / KIND_DGP weights and WGRAD gradients are N-major
+  constexpr bool B_MN = KIND != GEMM_FPROP && KIND != KIND_F4;  // DGRAD / KIND_DGP weights, WGRAD gradients: N-major
   constexpr int NB = seg_bufs(BN);
   constexpr uint32_t TMEM_COLS = NB * BN;
 
@@ -546,9 +558,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       constexpr uint32_t idesc = make_idesc(2 * BM, BN, A_MN, B_MN);
       // K-major SW128: 8-row atoms at 1024 B, K-step of 8 fp32 = +32 B inside the row.
       // MN-major SW128_BASE32B: 4-row atoms at 512 B along K, 32-wide MN atoms at 4096 B.
-      constexpr uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = A_MN ? 512u : 1024u, a_step = A_MN ? 1024u : 32u;
+      constexpr bool F4 = KIND == KIND_F4;
+      constexpr uint32_t a_lbo = A_MN ? 4096u : F4 ? 2048u : 16u, a_sbo = A_MN ? 512u : F4 ? 128u : 1024u,
+                         a_step = A_MN ? 1024u : F4 ? 4096u : 32u;
       constexpr uint32_t b_lbo = B_MN ? 4096u : 16u, b_sbo = B_MN ? 512u : 1024u, b_step = B_MN ? 1024u : 32u;
-      constexpr uint32_t a_lay = A_MN ? UMMA_SW128_BASE32B : UMMA_SW128;
+      constexpr uint32_t a_lay = A_MN ? UMMA_SW128_BASE32B : F4 ? UMMA_SW_NONE : UMMA_SW128;
       constexpr uint32_t b_lay = B_MN ? UMMA_SW128_BASE32B : UMMA_SW128;
       uint32_t it = 0, sc = 0;
       for (int t = cl; t < ntiles; t += ncl) {
@@ -842,7 +856,7 @@ cudaError_t launch_pair_bn(const CUtensorMap& ta, const CUtensorMap& tb, const P
   const int tiles = P.ntn * P.ntmp * P.nz;
   if (tiles == 0 || P.nk == 0) return cudaSuccess;
   const int pairs = std::min(tiles, sm_count_tma() / 2);
-  if constexpr (KIND != GEMM_WGRAD && BN <= 128 && MODE == MATH_TF32X3) {
+  if constexpr (KIND != GEMM_WGRAD && KIND != KIND_F4 && BN <= 128 && MODE == MATH_TF32X3) {
     if (atm_enabled())
       return P.stat_mode != STAT_NONE ? launch_pair_atm<KIND, BN, true>(ta, tb, P, 2 * pairs, st)
                                       : launch_pair_atm<KIND, BN, false>(ta, tb, P, 2 * pairs, st);
@@ -908,6 +922,11 @@ bool gemm_pair_supported(const GemmArgs& a) {
   }();
   if (disabled || !encode_fn() || sm_count_tma() < 2) return false;
   const ConvGeo& g = a.g;
+  static const bool no_f4 = [] {
+    const char* e = std::getenv("PG_NO_F4");
+    return e && std::atoi(e) != 0;
+  }();
+  if (a.kind == GEMM_FPROP && g.CG == 4 && no_f4) return false;
   if (g.s < 1 || g.s > 8 || g.k < 1) return false;
   if (a.kind == GEMM_FPROP && spatial_box(g.B, g.SH, g.SW, BM).TW * g.s > 256) return false;
   if (a.kind == GEMM_WGRAD && spatial_box(g.B, g.SH, g.SW, BKT).TW * g.s > 256) return false;
@@ -915,7 +934,8 @@ bool gemm_pair_supported(const GemmArgs& a) {
   if (!aligned16(a.out) || !aligned16(a.w) || a.out_ls % 4 || a.w_ls % 4) return false;
   switch (a.kind) {
     case GEMM_FPROP:
-      return g.CG % 32 == 0 && g.CS >= 64 && g.CS % 32 == 0 && aligned16(a.big) && a.big_ls % 4 == 0;
+      return (g.CG % 32 == 0 || (g.CG == 4 && (g.k * g.k * 4) % BKT == 0)) && g.CS >= 64 && g.CS % 32 == 0 &&
+             aligned16(a.big) && a.big_ls % 4 == 0;
     case GEMM_DGRAD:
       return g.CS % 32 == 0 && g.CG >= 64 && g.CG % 32 == 0 && aligned16(a.small) && a.small_ls % 4 == 0;
     default:
@@ -979,7 +999,24 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   const int sstr[5] = {1, g.s, g.s, 1, 1};
   bool ok = true;
   int bn, ntm = 1;
-  if (a.kind == GEMM_FPROP) {
+  const bool f4 = a.kind == GEMM_FPROP && g.CG == 4;
+  if (f4) {
+    P.N = g.CS;
+    P.kcb = 1;
+    P.nk = kk * 4 / BKT;
+    P.box = spatial_box(g.B, g.SH, g.SW, BM);
+    ntm = P.box.nb * P.box.ny * P.box.nx;
+    bn = pair_bn(P.N);
+    const long long ad[5] = {4, g.GW, g.GH, g.B, a.L};
+    const long long as[4] = {4, (long long)g.GW * 4, (long long)g.GH * g.GW * 4, a.big_ls};
+    const int abox[5] = {4, P.box.TW * g.s, P.box.TH * g.s, P.box.TB, 1};
+    ok = ok && make_map(&ta, a.big, 5, ad, as, abox, sstr, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const long long K = (long long)kk * 4;
+    const long long bd[3] = {K, g.CS, a.L};
+    const long long bs[2] = {K, a.w_ls};
+    const int bbox[3] = {BKT, bn / 2, 1};
+    ok = ok && make_map(&tb, a.w, 3, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if (a.kind == GEMM_FPROP) {
     P.N = g.CS;
     P.kcb = g.CG / BKT;
     P.nk = kk * P.kcb;
@@ -1077,6 +1114,9 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   if (dgrad_packed(a))
     return x3 ? launch_pair_kind<KIND_DGP, MATH_TF32X3>(ta, tb, P, bn, st)
               : launch_pair_kind<KIND_DGP, MATH_TF32>(ta, tb, P, bn, st);
+  if (f4)
+    return x3 ? launch_pair_kind<KIND_F4, MATH_TF32X3>(ta, tb, P, bn, st)
+              : launch_pair_kind<KIND_F4, MATH_TF32>(ta, tb, P, bn, st);
   switch (a.kind) {
     case GEMM_FPROP:
       return x3 ? launch_pair_kind<GEMM_FPROP, MATH_TF32X3>(ta, tb, P, bn, st)
