@@ -136,28 +136,40 @@ struct RowPix {
   }
 };
 
-// bias, padding columns (written 0) and activation of one output row
+// bias, padding columns (written 0) and activation of one output row, eight
+// columns per 256-bit store (one full 32-byte sector per lane: float4 stores
+// left every sector half-written twice); the next group's bias is loaded while
+// the current one is computed
 template <int ACT, int BH>
 PG_DEV void epi_store(const float (&acc)[BH], const RowPix& rp, float* out, int nb, const float* bias,
                       const PairPlan& P) {
   const bool padded = P.c_valid != P.c_pad;
+  float4 bn0 = make_float4(0.f, 0.f, 0.f, 0.f), bn1 = bn0;
+  if (bias && nb < P.N) {
+    bn0 = __ldg(reinterpret_cast<const float4*>(bias + rp.chan(nb)));
+    bn1 = __ldg(reinterpret_cast<const float4*>(bias + rp.chan(nb) + 4));
+  }
 #pragma unroll
-  for (int c4 = 0; c4 < BH; c4 += 4) {
-    const int n = nb + c4;
+  for (int c8 = 0; c8 < BH; c8 += 8) {
+    const int n = nb + c8;
     if (n >= P.N) break;
+    const float bb[8] = {bn0.x, bn0.y, bn0.z, bn0.w, bn1.x, bn1.y, bn1.z, bn1.w};
+    if (bias && c8 + 8 < BH && n + 8 < P.N) {
+      bn0 = __ldg(reinterpret_cast<const float4*>(bias + rp.chan(n + 8)));
+      bn1 = __ldg(reinterpret_cast<const float4*>(bias + rp.chan(n + 8) + 4));
+    }
     const long long a = rp.addr(n);
     if (a < 0) continue;
     const int ch = rp.chan(n);
-    float o[4];
+    float o[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      float x = acc[c4 + u];
-      if (bias) x += bias[ch + u];
+    for (int u = 0; u < 8; ++u) {
+      float x = acc[c8 + u] + bb[u];
       x = act_t<ACT>(x, P.slope);
       if (padded && (ch + u) % P.c_pad >= P.c_valid) x = 0.f;
       o[u] = x;
     }
-    *reinterpret_cast<float4*>(out + a) = make_float4(o[0], o[1], o[2], o[3]);
+    st_global_v8(out + a, o);
   }
 }
 
@@ -200,11 +212,7 @@ PG_DEV void epi_stats(const float (&acc)[BH], const RowPix& rp, float* out, int 
         v[u4 + 3] = act_bwd_rl(P.stat_act, v[u4 + 3], y4.w, P.stat_slope);
       }
     }
-    if (valid) {
-      float* crow = out + lo_off;
-      *reinterpret_cast<float4*>(crow) = make_float4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<float4*>(crow + 4) = make_float4(v[4], v[5], v[6], v[7]);
-    }
+    if (valid) st_global_v8(out + lo_off, v);
     float* s8 = st + n0;
     if (MODE == STAT_FWD) {
       // shifted sums around the slot's first row (lane 0), merged across slots
@@ -932,6 +940,8 @@ bool gemm_pair_supported(const GemmArgs& a) {
   if (a.kind == GEMM_WGRAD && spatial_box(g.B, g.SH, g.SW, BKT).TW * g.s > 256) return false;
   if (a.kind == GEMM_DGRAD && g.k % g.s) return false;
   if (!aligned16(a.out) || !aligned16(a.w) || a.out_ls % 4 || a.w_ls % 4) return false;
+  // FPROP / DGRAD epilogues store 8 columns per 256-bit store
+  if (a.kind != GEMM_WGRAD && ((reinterpret_cast<uintptr_t>(a.out) & 31) || a.out_ls % 8)) return false;
   switch (a.kind) {
     case GEMM_FPROP:
       return (g.CG % 32 == 0 || (g.CG == 4 && (g.k * g.k * 4) % BKT == 0)) && g.CS >= 64 && g.CS % 32 == 0 &&
