@@ -235,12 +235,21 @@ def main():
     step_flops = Lg * args.batch * flops_img
     peaks = measured_peaks()
     achieved = step_flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
-    # TF32 dense peak: half the measured bf16 dense burst figure
-    tf32_peak = peaks["bf16_tflops"] / 2.0
+    # denominator: this GPU's tcgen05 kind::tf32 dense rate, measured live by
+    # the pair-MMA probe (the driver's MEASURED_PEAKS.json holds a bf16 figure)
+    import ctypes as C
+    tf32_peak = C.c_double(0.0)
+    N.check(lib.pg_tc_tf32_peak(1 << 16, C.byref(tf32_peak)))
+    tf32_peak = tf32_peak.value
+    x3 = args.math == "tf32x3"
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                 "frac": (achieved / tf32_peak) if achieved else None, "traffic": None,
+                # 3xTF32 issues three MMAs per product: tensor-pipe occupancy is 3x the algorithmic fraction
+                "pipe_frac": (achieved * (3 if x3 else 1) / tf32_peak) if achieved else None,
                 "kernel": "implicit-GEMM (conv/convT/dense fwd, dgrad, wgrad), all launches of one step",
-                "peak_basis": f"tf32 dense = 1/2 x {peaks['source']} bf16 {peaks['bf16_tflops']} TF/s",
+                "peak_basis": "measured live: pg_tc_tf32_peak (cta_group::2 M256 N256 K8 kind::tf32 MMAs "
+                              "back to back on every SM pair)",
+                "bf16_dense_driver": peaks["bf16_tflops"],
                 "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / (max_ms / ran) if ran else None,
                 "algorithmic_flop_per_image": flops_img}
 

@@ -47,6 +47,10 @@ int pg_kernel_timing_read(double* gemm_ms);
 /* text report, one line per timed GEMM launch ("kind L= M= N= K= ... ms");
  * returns the full length (copies at most cap-1 bytes + NUL) */
 long pg_kernel_timing_report(char* out, long cap);
+/* measured tcgen05 kind::tf32 dense throughput of the current device (TFLOP/s):
+ * back-to-back CTA-pair M=256 N=256 K=8 MMAs from shared memory on every SM
+ * pair; the roofline denominator bench.py reports (not a reference interface) */
+int pg_tc_tf32_peak(int iters, double* tflops);
 
 /* Convolution geometry of one layer for one label: input map H x W x Cin,
  * output map OH x OW x Cout, square kernel k, stride s, padding p, batch B.

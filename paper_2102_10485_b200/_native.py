@@ -54,6 +54,7 @@ _SIGNATURES = {
     "pg_kernel_timing": (C.c_int, [C.c_int]),
     "pg_kernel_timing_read": (C.c_int, [C.POINTER(C.c_double)]),
     "pg_kernel_timing_report": (C.c_long, [C.c_char_p, C.c_long]),
+    "pg_tc_tf32_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "pg_conv2d_fwd": (C.c_int, [C.POINTER(ConvDesc), C.c_int, _P, _P, _LL, _P, _LL, C.c_int, C.c_float, _P, C.c_int, _P]),
     "pg_conv2d_bwd_data": (C.c_int, [C.POINTER(ConvDesc), C.c_int, _P, _P, _LL, _P, C.c_int, _P]),
     "pg_conv2d_bwd_filter": (C.c_int, [C.POINTER(ConvDesc), C.c_int, _P, _P, _P, _LL, C.c_int, C.c_int, _P]),

@@ -109,6 +109,10 @@ int pg_kernel_timing_read(double* ms) {
   return guard([&] { *ms = pg::gemm_timing_read_ms(); });
 }
 
+int pg_tc_tf32_peak(int iters, double* tflops) {
+  return guard([&] { pg::check_cuda(pg::tc_tf32_peak(iters, tflops), "tc peak"); });
+}
+
 long pg_kernel_timing_report(char* out, long cap) {
   std::string r = pg::gemm_timing_report();
   if (out && cap > 0) {

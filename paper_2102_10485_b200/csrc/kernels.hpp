@@ -20,6 +20,8 @@ double gemm_timing_read_ms();
 namespace pg {
 std::string gemm_timing_report();  // one line per timed GEMM launch: shape tags + ms
 
+// measured tcgen05 kind::tf32 dense peak (TFLOP/s), tc_peak.cu
+cudaError_t tc_tf32_peak(int iters, double* tflops);
 int gemm_max_m(const GemmArgs& a);
 int gemm_n(const GemmArgs& a);
 cudaError_t launch_gemm_simt(const GemmArgs& a, cudaStream_t st);
