@@ -12,52 +12,69 @@ namespace pg {
 
 namespace {
 
-constexpr int RED_ROWS = 128;  // rows per reduction chunk
-constexpr int RED_TY = 8;      // row lanes per block (block = 32 channels x 8)
+constexpr int RED_ROWS = 512;  // rows per reduction chunk
+constexpr int RED_NT = 256;
 
-__global__ void channel_reduce_kernel(ChannelMap cm, int mode, const float* __restrict__ x,
-                                      const float* __restrict__ gy, const float* __restrict__ y,
-                                      const float* __restrict__ mean, int act, float slope,
-                                      float* __restrict__ partial) {
-  const int l = blockIdx.z, chunk = blockIdx.x;
-  const int c = blockIdx.y * 32 + threadIdx.x;
-  const int nchunk = gridDim.x;
-  const long long base = (long long)l * cm.ls;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-  if (c < cm.Cp) {
-    const float mu = (mode == RED_SQDEV || mode == RED_BN_BWD) ? mean[(long long)l * cm.Cp + c] : 0.f;
+PG_DEV float4 f4(float v) { return make_float4(v, v, v, v); }
+PG_DEV float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+PG_DEV float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// Per-channel sums over the rows of [L][R][Cp] maps.  Block = (label, chunk of
+// RED_ROWS rows, up to 256 float4 channel groups): a thread owns 4 channels
+// (float4 loads along the row) and a row lane; the row lanes are combined in
+// shared memory in a fixed order, and the chunk partials by the finalize
+// kernels in chunk order (deterministic, no atomics).
+__global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, int mode, const float* __restrict__ x,
+                                                                const float* __restrict__ gy,
+                                                                const float* __restrict__ y,
+                                                                const float* __restrict__ mean, int act, float slope,
+                                                                float* __restrict__ partial) {
+  const int l = blockIdx.z, chunk = blockIdx.x, nchunk = gridDim.x;
+  const int c4n = cm.Cp / 4;
+  const int gpb = c4n < RED_NT ? c4n : RED_NT;  // channel groups per block
+  const int lanes = RED_NT / gpb;
+  const int t = threadIdx.x, gi = t % gpb, lr = t / gpb;
+  const int g = blockIdx.y * gpb + gi;
+  float4 s0 = f4(0.f), s1 = f4(0.f), s2 = f4(0.f);
+  if (g < c4n && lr < lanes) {
+    const float4 mu = (mode == RED_SQDEV || mode == RED_BN_BWD) ? ld4(mean + (long long)l * cm.Cp + 4 * g) : f4(0.f);
+    const long long base = (long long)l * cm.ls + 4 * g;
     const int r_end = min(cm.R, (chunk + 1) * RED_ROWS);
-    for (int r = chunk * RED_ROWS + threadIdx.y; r < r_end; r += RED_TY) {
-      const long long o = base + (long long)r * cm.Cp + c;
-      switch (mode) {
-        case RED_SUM: s0 += x[o]; break;
-        case RED_SQDEV: {
-          float d = x[o] - mu;
-          s0 += d * d;
-          break;
+#pragma unroll 4
+    for (int r = chunk * RED_ROWS + lr; r < r_end; r += lanes) {
+      const long long o = base + (long long)r * cm.Cp;
+      if (mode == RED_SUM) {
+        s0 = add4(s0, ld4(x + o));
+      } else if (mode == RED_SQDEV) {
+        const float4 v = ld4(x + o);
+        const float dx = v.x - mu.x, dy = v.y - mu.y, dz = v.z - mu.z, dw = v.w - mu.w;
+        s0 = add4(s0, make_float4(dx * dx, dy * dy, dz * dz, dw * dw));
+      } else {
+        const float4 g4 = ld4(gy + o), y4 = ld4(y + o);
+        const float4 g1 = make_float4(act_bwd(act, g4.x, y4.x, slope), act_bwd(act, g4.y, y4.y, slope),
+                                      act_bwd(act, g4.z, y4.z, slope), act_bwd(act, g4.w, y4.w, slope));
+        s0 = add4(s0, g1);
+        if (mode == RED_BN_BWD) {
+          const float4 v = ld4(x + o);
+          const float4 d = make_float4(v.x - mu.x, v.y - mu.y, v.z - mu.z, v.w - mu.w);
+          s1 = add4(s1, make_float4(g1.x * d.x, g1.y * d.y, g1.z * d.z, g1.w * d.w));
+          s2 = add4(s2, d);
         }
-        case RED_BN_BWD: {
-          float g1 = act_bwd(act, gy[o], y[o], slope);
-          float d = x[o] - mu;
-          s0 += g1;
-          s1 += g1 * d;
-          s2 += d;
-          break;
-        }
-        default: s0 += act_bwd(act, gy[o], y[o], slope); break;
       }
     }
   }
-  __shared__ float sm[3][RED_TY][33];
-  sm[0][threadIdx.y][threadIdx.x] = s0;
-  sm[1][threadIdx.y][threadIdx.x] = s1;
-  sm[2][threadIdx.y][threadIdx.x] = s2;
+  __shared__ float4 sm[3][RED_NT];
+  sm[0][t] = s0;
+  sm[1][t] = s1;
+  sm[2][t] = s2;
   __syncthreads();
-  if (threadIdx.y < 3 && c < cm.Cp) {
-    float t = 0.f;
-#pragma unroll
-    for (int i = 0; i < RED_TY; ++i) t += sm[threadIdx.y][i][threadIdx.x];
-    partial[(((long long)l * nchunk + chunk) * 3 + threadIdx.y) * cm.Cp + c] = t;
+  if (lr != 0 || g >= c4n) return;
+  const int nk = mode == RED_BN_BWD ? 3 : 1;
+  for (int k = 0; k < 3; ++k) {
+    float4 acc = f4(0.f);
+    if (k < nk)
+      for (int i = 0; i < lanes; ++i) acc = add4(acc, sm[k][i * gpb + gi]);
+    *reinterpret_cast<float4*>(partial + (((long long)l * nchunk + chunk) * 3 + k) * cm.Cp + 4 * g) = acc;
   }
 }
 
@@ -182,15 +199,45 @@ __global__ void bn_eval_stats_kernel(ChannelMap cm, const float* running, long l
   }
 }
 
-// float4 over [L][R][Cp] (Cp % 4 == 0)
-__global__ void bn_apply_kernel(ChannelMap cm, const float* __restrict__ x, const float* __restrict__ mean,
-                                const float* __restrict__ istd, const float* __restrict__ gb, long long gb_ls, int act,
-                                float slope, float* __restrict__ y) {
-  const long long per = (long long)cm.R * cm.Cp / 4;
+// float4 over [L][R][Cp] (Cp % 4 == 0).  When the grid stride is a multiple of
+// the row width (the usual case: Cp / 4 divides 256), each thread keeps one
+// channel group for all its elements and holds its coefficients in registers.
+__global__ void __launch_bounds__(256) bn_apply_kernel(ChannelMap cm, const float* __restrict__ x,
+                                                       const float* __restrict__ mean, const float* __restrict__ istd,
+                                                       const float* __restrict__ gb, long long gb_ls, int act,
+                                                       float slope, float* __restrict__ y) {
+  const int c4n = cm.Cp / 4;
+  const long long per = (long long)cm.R * c4n;
   const int l = blockIdx.y;
   const float* gamma = gb + (long long)l * gb_ls;
   const float* beta = gamma + cm.C;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < per; q += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long q0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (stride % c4n == 0) {
+    const int c0 = (int)(q0 % c4n) * 4;
+    float a[4], m[4], bb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u;
+      const long long mc = (long long)l * cm.Cp + c;
+      const bool ok = c < cm.C;
+      a[u] = ok ? gamma[c] * istd[mc] : 0.f;
+      m[u] = ok ? mean[mc] : 0.f;
+      bb[u] = ok ? beta[c] : 0.f;
+    }
+    for (long long q = q0; q < per; q += stride) {
+      const long long o = (long long)l * cm.ls + q * 4;
+      const float4 v = *reinterpret_cast<const float4*>(x + o);
+      const float r[4] = {v.x, v.y, v.z, v.w};
+      float o4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        o4[u] = c0 + u < cm.C ? act_fwd(act, a[u] * (r[u] - m[u]) + bb[u], slope) : 0.f;
+      *reinterpret_cast<float4*>(y + o) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+    }
+    return;
+  }
+  for (long long q = q0; q < per; q += stride) {
     const long long o = (long long)l * cm.ls + q * 4;
     const int c0 = (int)((q * 4) % cm.Cp);
     float4 v = *reinterpret_cast<const float4*>(x + o);
@@ -200,7 +247,7 @@ __global__ void bn_apply_kernel(ChannelMap cm, const float* __restrict__ x, cons
       int c = c0 + u;
       if (c < cm.C) {
         long long mc = (long long)l * cm.Cp + c;
-        r[u] = act_fwd(act, gamma[c] * ((r[u] - mean[mc]) * istd[mc]) + beta[c], slope);
+        r[u] = act_fwd(act, gamma[c] * istd[mc] * (r[u] - mean[mc]) + beta[c], slope);
       } else {
         r[u] = 0.f;
       }
@@ -474,8 +521,10 @@ size_t reduce_partial_floats(const ChannelMap& cm) { return (size_t)cm.L * reduc
 
 cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x, const float* gy, const float* y,
                                   const float* mean, int act, float slope, float* partial, cudaStream_t st) {
-  dim3 grid(reduce_chunks(cm.R), (cm.Cp + 31) / 32, cm.L);
-  channel_reduce_kernel<<<grid, dim3(32, RED_TY), 0, st>>>(cm, mode, x, gy, y, mean, act, slope, partial);
+  if (cm.Cp % 4) return cudaErrorInvalidValue;
+  const int c4n = cm.Cp / 4, gpb = c4n < RED_NT ? c4n : RED_NT;
+  dim3 grid(reduce_chunks(cm.R), (c4n + gpb - 1) / gpb, cm.L);
+  channel_reduce_kernel<<<grid, RED_NT, 0, st>>>(cm, mode, x, gy, y, mean, act, slope, partial);
   return launched();
 }
 

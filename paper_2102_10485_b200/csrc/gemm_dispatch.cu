@@ -25,9 +25,15 @@ bool lowered_enabled(const GemmArgs& a) {
   }();
   return !(off & (a.kind == GEMM_FPROP ? 1 : 2));
 }
-// the 4-channel image-side FPROP runs on the pair engine's direct TMA gather
-// (KIND_F4) ahead of the SIMT thin kernel
-bool image_side_direct(const GemmArgs& a) { return a.kind == GEMM_FPROP && a.g.CG == 4 && gemm_pair_supported(a); }
+// FPROP shapes the SIMT thin kernels also accept but the pair engine runs
+// faster: the 4-channel image side (direct TMA gather, KIND_F4) and wide dense
+// layers with a small K (the generator's latent projection, K = 100)
+bool image_side_direct(const GemmArgs& a) {
+  if (a.kind != GEMM_FPROP) return false;
+  const ConvGeo& g = a.g;
+  const bool dense = g.k == 1 && g.SH == 1 && g.SW == 1 && g.GH == 1 && g.GW == 1;
+  return (g.CG == 4 || (dense && g.CS >= 64)) && gemm_pair_supported(a);
+}
 }  // namespace
 
 std::string gemm_timing_report() {

@@ -884,6 +884,10 @@ cudaError_t launch_pair_kind(const CUtensorMap& ta, const CUtensorMap& tb, const
 
 int pair_bn(int n) { return n >= 256 ? 256 : n >= 128 ? 128 : 64; }
 
+bool dense_1x1(const ConvGeo& g) {
+  return g.k == 1 && g.s == 1 && g.p == 0 && g.SH == 1 && g.SW == 1 && g.GH == 1 && g.GW == 1;
+}
+
 // Base grid of the phase-packed DGRAD is (H/2 + 1) x (W/2 + 1) (17 x 17 for a
 // 32 x 32 output): a power-of-two box would waste half the rows, so the box
 // is W wide (whole rows) and at most 128 rows deep, picking the TH x TB split
@@ -944,8 +948,9 @@ bool gemm_pair_supported(const GemmArgs& a) {
   if (a.kind != GEMM_WGRAD && ((reinterpret_cast<uintptr_t>(a.out) & 31) || a.out_ls % 8)) return false;
   switch (a.kind) {
     case GEMM_FPROP:
-      return (g.CG % 32 == 0 || (g.CG == 4 && (g.k * g.k * 4) % BKT == 0)) && g.CS >= 64 && g.CS % 32 == 0 &&
-             aligned16(a.big) && a.big_ls % 4 == 0;
+      // K tail of a dense layer (e.g. the latent width 100) is zero-filled by TMA out-of-bounds reads
+      return (g.CG % 32 == 0 || (g.CG == 4 && (g.k * g.k * 4) % BKT == 0) || (dense_1x1(g) && g.CG % 4 == 0)) &&
+             g.CS >= 64 && g.CS % 32 == 0 && aligned16(a.big) && a.big_ls % 4 == 0;
     case GEMM_DGRAD:
       return g.CS % 32 == 0 && g.CG >= 64 && g.CG % 32 == 0 && aligned16(a.small) && a.small_ls % 4 == 0;
     default:
@@ -1028,7 +1033,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
     ok = ok && make_map(&tb, a.w, 3, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B);
   } else if (a.kind == GEMM_FPROP) {
     P.N = g.CS;
-    P.kcb = g.CG / BKT;
+    P.kcb = (g.CG + BKT - 1) / BKT;
     P.nk = kk * P.kcb;
     P.box = spatial_box(g.B, g.SH, g.SW, BM);
     ntm = P.box.nb * P.box.ny * P.box.nx;

@@ -515,6 +515,9 @@ void DevNet::forward(Trace& t, int B, bool train, bool update_running, cudaStrea
                   static_cast<int>(b.out.C), static_cast<long long>(B) * b.out.numel()};
     int npack = 1;
     const int slots = train && fuse_enabled(1) ? gemm_stat_slots(a, math_, &npack) : 0;
+    // a dense layer reshaped to [C][H][W] before BatchNorm: GEMM column n is
+    // (pixel, channel) -> H*W statistic columns per channel
+    if (npack == 1) npack = gemm_n(a) / static_cast<int>(b.out.Cp);
     if (slots > 0) {
       // batch statistics fused into the GEMM epilogue (per 32-row slot), merged here
       a.stat_mode = STAT_FWD;

@@ -240,12 +240,14 @@ def test_dense_fwd_bwd_with_activation(native, oracle, torch_cuda, math, tol):
 
 
 @pytest.mark.parametrize("act,spec_act", [(1, "relu"), (2, "lrelu 0.2")])
-def test_batchnorm_fwd_bwd_train(native, oracle, torch_cuda, act, spec_act):
+@pytest.mark.parametrize("L,B,Cch,H,W", [(2, 6, 6, 5, 5), (2, 16, 128, 8, 8), (3, 40, 64, 7, 7), (2, 16, 256, 4, 4)])
+def test_batchnorm_fwd_bwd_train(native, oracle, torch_cuda, act, spec_act, L, B, Cch, H, W):
     """BN over an NHWC map with the fused activation; statistics, running-stat
-    update, dgamma/dbeta and the input gradient vs the oracle (1e-5)."""
+    update, dgamma/dbeta and the input gradient vs the oracle (1e-5).  Shapes
+    cover one and several 512-row reduction chunks (ragged last chunk) and
+    several labels."""
     from paper_2102_10485_b200 import _native as N
     torch = torch_cuda
-    L, B, Cch, H, W = 2, 6, 6, 5, 5
     Cp = pad4(Cch)
     spec = f"bn {Cch}; {spec_act}"
     rng = np.random.default_rng(9)
