@@ -6,6 +6,7 @@
 // fixed-order second pass over the chunk partials (no float atomics).
 #include "kernels.hpp"
 
+#include <algorithm>
 #include <cmath>
 
 namespace pg {
@@ -225,16 +226,26 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(ChannelMap cm, const floa
       m[u] = ok ? mean[mc] : 0.f;
       bb[u] = ok ? beta[c] : 0.f;
     }
-    for (long long q = q0; q < per; q += stride) {
-      const long long o = (long long)l * cm.ls + q * 4;
-      const float4 v = *reinterpret_cast<const float4*>(x + o);
+    const float* xl = x + (long long)l * cm.ls;
+    float* yl = y + (long long)l * cm.ls;
+    auto apply = [&](float4 v) {
       const float r[4] = {v.x, v.y, v.z, v.w};
       float o4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         o4[u] = c0 + u < cm.C ? act_fwd(act, a[u] * (r[u] - m[u]) + bb[u], slope) : 0.f;
-      *reinterpret_cast<float4*>(y + o) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+      return make_float4(o4[0], o4[1], o4[2], o4[3]);
+    };
+    long long q = q0;
+    // four independent float4 loads in flight per thread
+    for (; q + 3 * stride < per; q += 4 * stride) {
+      float4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = ld4(xl + (q + k * stride) * 4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) *reinterpret_cast<float4*>(yl + (q + k * stride) * 4) = apply(v[k]);
     }
+    for (; q < per; q += stride) *reinterpret_cast<float4*>(yl + q * 4) = apply(ld4(xl + q * 4));
     return;
   }
   for (long long q = q0; q < per; q += stride) {
@@ -552,7 +563,11 @@ cudaError_t launch_bn_eval_stats(const ChannelMap& cm, const float* running, lon
 
 cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* mean, const float* istd,
                             const float* gamma_beta, long long gb_ls, int act, float slope, float* y, cudaStream_t st) {
-  dim3 grid(grid_for((long long)cm.R * cm.Cp / 4, 256, 4096), cm.L);
+  // few fat threads: each keeps its channel coefficients in registers and
+  // streams ~16 float4 (8 blocks per SM over all labels)
+  const long long per = (long long)cm.R * cm.Cp / 4;
+  const unsigned cap = std::max(1u, 148u * 8u / (unsigned)std::max(1, cm.L));
+  dim3 grid(grid_for(per, 256 * 16, cap), cm.L);
   bn_apply_kernel<<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y);
   return launched();
 }

@@ -48,6 +48,11 @@ constexpr int NT = (4 + NDRAIN) * 32;
 constexpr int W_MMA = 3, W_DRAIN = 4;
 constexpr int SMEM_BUDGET = 200 * 1024;
 constexpr int KIND_DGP = 3;  // phase-packed stride-2 DGRAD (k = 4, s = 2, p = 1), engine-internal
+// widest packed N: packing CG = 128 (N = 512) measured 1.36 vs 1.22 ms on the
+// 16x16 layer (the 9x9 base grid wastes 27% of the rows), CG = 256: 1.75 vs 0.98
+#ifndef PG_DGP_MAXN
+#define PG_DGP_MAXN 256
+#endif
 constexpr int KIND_F4 = 4;   // FPROP from a 4-channel (padded RGB) map: a k-block = 8 taps x 4 channels
 #ifndef PG_PAIR_SL
 #define PG_PAIR_SL 0
@@ -922,7 +927,7 @@ bool dgrad_packed(const GemmArgs& a) {
   }();
   const ConvGeo& g = a.g;
   return !disabled && a.kind == GEMM_DGRAD && g.k == 4 && g.s == 2 && g.p == 1 && g.GH == 2 * g.SH &&
-         g.GW == 2 * g.SW && g.CG % 32 == 0 && 4 * g.CG <= 256 && g.CS % 32 == 0;
+         g.GW == 2 * g.SW && g.CG % 32 == 0 && 4 * g.CG <= PG_DGP_MAXN && g.CS % 32 == 0;
 }
 
 }  // namespace
