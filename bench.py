@@ -242,8 +242,15 @@ def main():
     N.check(lib.pg_tc_tf32_peak(1 << 16, C.byref(tf32_peak)))
     tf32_peak = tf32_peak.value
     x3 = args.math == "tf32x3"
+    # DRAM bytes of the step's implicit-GEMM launches, from the committed ncu launch list
+    traffic = None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("gemm_dram_bytes_per_step")
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
-                "frac": (achieved / tf32_peak) if achieved else None, "traffic": None,
+                "frac": (achieved / tf32_peak) if achieved else None, "traffic": traffic,
+                "traffic_unit": "bytes per step (all implicit-GEMM launches, ncu dram__bytes_read + write)",
                 # 3xTF32 issues three MMAs per product: tensor-pipe occupancy is 3x the algorithmic fraction
                 "pipe_frac": (achieved * (3 if x3 else 1) / tf32_peak) if achieved else None,
                 "kernel": "implicit-GEMM (conv/convT/dense fwd, dgrad, wgrad), all launches of one step",
