@@ -74,6 +74,10 @@ int pg_group_set(pg_group* g, int label_index, int field, const double* in, long
 int pg_group_failed(pg_group* g, int* failed);
 /* eval-mode samples for every label: latents from Rng(derive_seed(seed, class_id)); out [n_labels][n][C][H][W] in [0,1] */
 int pg_group_generate(pg_group* g, long n, uint64_t seed, float* out);
+/* mixture_sample (include/partgan/partition.hpp, src/partition.cpp:182-227) over the
+ * group's labels in order: priors[n_labels]; class ids then per-class latents drawn
+ * from Rng(seed) exactly as the reference; out [n][C][H][W] in [0,1], ids[n] */
+int pg_group_mixture_sample(pg_group* g, const double* priors, long n, uint64_t seed, float* out, int* ids);
 /* device time (ms, CUDA events) of the last pg_group_train_steps call */
 float pg_group_last_ms(pg_group* g);
 int pg_group_sync(pg_group* g);

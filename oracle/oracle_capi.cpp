@@ -21,6 +21,8 @@ struct GroupBase {
   virtual void set(int l, int what, const double* in, long n) = 0;
   virtual void step_inputs(int l, const double* real01, const double* z1, const double* z2, long B, double* rep) = 0;
   virtual int labels() const = 0;
+  // mixture_sample (partition.cpp:182-227) over the group's pairs in label order
+  virtual void mixture(const double* priors, long n, uint64_t seed, double* out, int* ids) = 0;
 };
 
 template <class R>
@@ -105,6 +107,17 @@ struct Group : GroupBase {
       case 3: take(p.disc.buffers, in, n); return;
     }
     throw std::invalid_argument("field not settable: " + std::to_string(what));
+  }
+
+  void mixture(const double* priors, long n, uint64_t seed, double* out, int* ids) override {
+    std::vector<const GanPair<R>*> pairs;
+    for (auto& k : w) pairs.push_back(&k->pair);
+    ClassPrior pri;
+    pri.probabilities.assign(priors, priors + w.size());
+    Rng rng(seed);
+    auto ms = mixture_sample<R>(pairs, pri, n, rng);
+    for (long i = 0; i < ms.first.size(); ++i) out[i] = static_cast<double>(ms.first[i]);
+    for (long i = 0; i < n; ++i) ids[i] = ms.second[static_cast<size_t>(i)];
   }
 
   void step_inputs(int l, const double* real01, const double* z1, const double* z2, long B, double* rep) override {
@@ -246,6 +259,11 @@ int or_group_set(void* h, int label_idx, int what, const double* in, long n) {
 int or_group_step_inputs(void* h, int label_idx, const double* real01, const double* z1, const double* z2, long B,
                          double* report4) {
   return guard([&] { static_cast<GroupBase*>(h)->step_inputs(label_idx, real01, z1, z2, B, report4); });
+}
+
+// n samples [n][C][H][W] in [0,1] and their class indices (group label order)
+int or_group_mixture(void* h, const double* priors, long n, uint64_t seed, double* out, int* ids) {
+  return guard([&] { static_cast<GroupBase*>(h)->mixture(priors, n, seed, out, ids); });
 }
 
 void or_group_destroy(void* h) { delete static_cast<GroupBase*>(h); }

@@ -473,6 +473,9 @@ int pg_group_failed(pg_group* g, int* failed) {
   });
 }
 int pg_group_generate(pg_group* g, long n, uint64_t seed, float* out) { return WITH_GROUP(grp.generate(n, seed, out)); }
+int pg_group_mixture_sample(pg_group* g, const double* priors, long n, uint64_t seed, float* out, int* ids) {
+  return WITH_GROUP(grp.mixture_sample(priors, n, seed, out, ids));
+}
 float pg_group_last_ms(pg_group* g) { return g ? G(g)->g->last_device_ms() : -1.f; }
 int pg_group_sync(pg_group* g) { return WITH_GROUP(grp.sync()); }
 int pg_group_sizes(pg_group* g, long long* out) {

@@ -475,4 +475,68 @@ void GanGroup::generate(long n, uint64_t seed, float* out) {
   }
 }
 
+void GanGroup::mixture_sample(const double* priors, long n, uint64_t seed, float* out, int* ids) {
+  if (n < 1) throw std::invalid_argument("mixture_sample: n must be >= 1");
+  sync();
+  const int k = L_;
+  Rng rng(seed);
+  // 1) class ids from one stream (partition.cpp:192-205); a single pair draws none
+  if (k == 1) {
+    std::fill(ids, ids + n, 0);
+  } else {
+    std::vector<double> cdf(static_cast<size_t>(k));
+    double acc = 0;
+    for (int j = 0; j < k; ++j) cdf[static_cast<size_t>(j)] = (acc += priors[j]);
+    for (long i = 0; i < n; ++i) {
+      const double u = rng.uniform();
+      int j = 0;
+      while (j + 1 < k && u >= cdf[static_cast<size_t>(j)]) ++j;
+      ids[i] = j;
+    }
+  }
+  // 2) per class, in class order, the latents of its samples from the same
+  //    stream (generate -> sample_latent, gan.cpp:54-84,197-201)
+  std::vector<std::vector<long>> where(static_cast<size_t>(k));
+  for (long i = 0; i < n; ++i) where[static_cast<size_t>(ids[i])].push_back(i);
+  std::vector<std::vector<float>> z(static_cast<size_t>(k));
+  long most = 0;
+  for (int j = 0; j < k; ++j) {
+    const long c = static_cast<long>(where[static_cast<size_t>(j)].size());
+    most = std::max(most, c);
+    z[static_cast<size_t>(j)].resize(static_cast<size_t>(c * cfg_.d_z));
+    for (auto& v : z[static_cast<size_t>(j)]) v = static_cast<float>(rng.normal());
+  }
+  // 3) device: all labels' generators in lockstep rounds of up to Bmax samples
+  const int Bmax = static_cast<int>(std::min<long>(cfg_.batch, cfg_.per_label));
+  const Map& om = G_->out_map();
+  const long S = cfg_.C * cfg_.H * cfg_.W;
+  DeviceBuf o(static_cast<size_t>(L_) * Bmax * S);
+  std::vector<float> zh(static_cast<size_t>(L_) * Bmax * zcp_), oh(o.n);
+  for (long done = 0; done < most; done += Bmax) {
+    const int B = static_cast<int>(std::min<long>(Bmax, most - done));
+    std::fill(zh.begin(), zh.end(), 0.f);
+    for (int l = 0; l < L_; ++l) {
+      const long c = static_cast<long>(where[static_cast<size_t>(l)].size());
+      for (int b = 0; b < B && done + b < c; ++b)
+        std::memcpy(&zh[(static_cast<size_t>(l) * B + b) * zcp_], &z[static_cast<size_t>(l)][(done + b) * cfg_.d_z],
+                    sizeof(float) * cfg_.d_z);
+    }
+    check_cuda(cudaMemcpyAsync(dz_[0][0].p, zh.data(), sizeof(float) * L_ * B * zcp_, cudaMemcpyHostToDevice, st_), "z");
+    tg_.act[0] = dz_[0][0].p;
+    G_->forward(tg_, B, false, false, st_);
+    check_cuda(launch_nhwc_to_nchw01(static_cast<long long>(L_) * B, static_cast<int>(cfg_.C), static_cast<int>(cfg_.H),
+                                     static_cast<int>(cfg_.W), static_cast<int>(om.Cp),
+                                     tg_.act[static_cast<size_t>(G_->blocks())], o.p, st_),
+               "to nchw");
+    check_cuda(cudaMemcpyAsync(oh.data(), o.p, sizeof(float) * L_ * B * S, cudaMemcpyDeviceToHost, st_), "samples D2H");
+    check_cuda(cudaStreamSynchronize(st_), "sync");
+    for (int l = 0; l < L_; ++l) {
+      const auto& wl = where[static_cast<size_t>(l)];
+      for (int b = 0; b < B && done + b < static_cast<long>(wl.size()); ++b)
+        std::memcpy(out + wl[static_cast<size_t>(done + b)] * S, oh.data() + (static_cast<size_t>(l) * B + b) * S,
+                    sizeof(float) * S);
+    }
+  }
+}
+
 }  // namespace pg

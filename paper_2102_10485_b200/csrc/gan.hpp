@@ -74,6 +74,10 @@ class GanGroup {
   // eval-mode samples: n per label with latents from Rng(derive_seed(seed, class_id)),
   // (v+1)/2 mapped, out [L][n][C][H][W]
   void generate(long n, uint64_t seed, float* out);
+  // mixture_sample (partition.cpp:182-227) over the group's labels in order:
+  // class ids and latents drawn on the host from Rng(seed) in the reference
+  // order, eval-mode generators on the device; out [n][C][H][W] in [0,1]
+  void mixture_sample(const double* priors, long n, uint64_t seed, float* out, int* ids);
   void sync();
   long steps_done() const { return steps_; }
 

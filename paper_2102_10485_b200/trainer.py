@@ -159,6 +159,20 @@ class LabelGroup:
         N.check(N.lib().pg_group_generate(self._h, n, seed, _fptr(out)), "generate")
         return out
 
+    def mixture_sample(self, priors, n: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
+        """mixture_sample (partition.cpp:182-227) over this group's labels in
+        order: (samples [n][C][H][W] in [0,1], class indices [n])."""
+        import ctypes as C
+        c, h, w = self.spec.arch.image
+        pri = np.ascontiguousarray(priors, np.float64)
+        if pri.shape != (self.n_labels,):
+            raise ValueError("mixture_sample: prior length does not match pair count")
+        out = np.zeros((n, c, h, w), np.float32)
+        ids = np.zeros(n, np.int32)
+        N.check(N.lib().pg_group_mixture_sample(self._h, pri.ctypes.data_as(C.POINTER(C.c_double)), n, seed,
+                                                _fptr(out), ids.ctypes.data_as(C.POINTER(C.c_int))), "mixture_sample")
+        return out, ids
+
     def sizes(self) -> dict:
         out = (C.c_longlong * 4)()
         N.check(N.lib().pg_group_sizes(self._h, out), "sizes")

@@ -39,6 +39,7 @@ def lib() -> C.CDLL:
         h.or_group_set.argtypes = [P, C.c_int, C.c_int, D, C.c_long]
         h.or_group_step_inputs.argtypes = [P, C.c_int, D, D, D, C.c_long, D]
         h.or_group_destroy.argtypes = [P]
+        h.or_group_mixture.argtypes = [P, D, C.c_long, C.c_uint64, D, C.POINTER(C.c_int)]
         h.or_dataset_label.argtypes = [C.c_long, C.c_long, C.c_long, C.c_int, C.c_long, C.c_uint64, D]
         h.or_derive_seed.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]
         h.or_partition.argtypes = [C.POINTER(C.c_int), C.c_long, C.c_int, C.POINTER(C.c_long), C.POINTER(C.c_long)]
@@ -89,6 +90,14 @@ class OracleGroup:
     def set(self, label: int, what: int, v: np.ndarray) -> None:
         v = np.ascontiguousarray(v, np.float64)
         check(lib().or_group_set(self.h, label, what, _d(v), v.size))
+
+    def mixture(self, priors, n: int, seed: int, sample_shape) -> tuple[np.ndarray, np.ndarray]:
+        """mixture_sample (partition.cpp:182-227) over the group's pairs: samples in [0,1], class indices."""
+        pri = np.ascontiguousarray(priors, np.float64)
+        out = np.zeros((n, *sample_shape), np.float64)
+        ids = np.zeros(n, np.int32)
+        check(lib().or_group_mixture(self.h, _d(pri), n, seed, _d(out), ids.ctypes.data_as(C.POINTER(C.c_int))))
+        return out, ids
 
     def step_inputs(self, label: int, real01: np.ndarray, z1: np.ndarray, z2: np.ndarray) -> np.ndarray:
         r = np.ascontiguousarray(real01, np.float64)

@@ -271,3 +271,29 @@ def test_generate_eval_mode(oracle):
     assert np.array_equal(a, b)
     assert a.min() >= 0 and a.max() <= 1
     assert a.std() > 0
+
+
+@pytest.mark.parametrize("math", [0, 1])
+def test_mixture_sample_matches_reference_protocol(oracle, math):
+    """mixture_sample (partition.cpp:182-227) after one training step of c1 on
+    three labels: class indices bit-exact (same stream: ids first, then each
+    class's latents in class order), samples within 1e-4 of the f64 oracle's
+    eval-mode generators (tanh range mapped to [0,1]).  Also the single-pair
+    case, which must draw no class ids (test_partition.cpp:196-210)."""
+    arch, grp = make_pair(1, 3, 128, 64, math)
+    orc = oracle.OracleGroup(64, 1, 3, 128, 64, data_seed=3, base_seed=7)
+    grp.train_steps(1)
+    orc.step(1)
+    pri = np.array([0.5, 0.2, 0.3])
+    for n, seed in ((200, 11), (37, 12)):
+        s, ids = grp.mixture_sample(pri, n, seed)
+        rs, rids = orc.mixture(pri, n, seed, arch.image)
+        assert np.array_equal(ids, rids)
+        assert set(np.unique(ids)) <= {0, 1, 2}
+        assert np.abs(s - rs).max() <= 1e-4 * max(1.0, np.abs(rs).max())
+    one_g = LabelGroup(GroupSpec(arch=arch, class_ids=[1], batch=64, per_label=128, base_seed=7, math=math))
+    one_o = oracle.OracleGroup(64, 1, 1, 128, 64, first_label=1, data_seed=3, base_seed=7)
+    s, ids = one_g.mixture_sample(np.array([1.0]), 50, 21)
+    rs, rids = one_o.mixture(np.array([1.0]), 50, 21, arch.image)
+    assert np.all(ids == 0) and np.array_equal(ids, rids)
+    assert np.abs(s - rs).max() <= 1e-4
