@@ -77,6 +77,12 @@ int pg_group_generate(pg_group* g, long n, uint64_t seed, float* out);
 /* mixture_sample (include/partgan/partition.hpp, src/partition.cpp:182-227) over the
  * group's labels in order: priors[n_labels]; class ids then per-class latents drawn
  * from Rng(seed) exactly as the reference; out [n][C][H][W] in [0,1], ids[n] */
+/* one label's (G, D) pair to / from a checkpoint file in the reference format
+ * (src/checkpoint.cpp:91-194 save_gan_pair / load_gan_pair: u32 LE header length,
+ * JSON header, f64 LE blobs gen_params, gen_buffers, disc_params, disc_buffers,
+ * opt_g_m, opt_g_v, opt_d_m, opt_d_v); load requires the group's architecture */
+int pg_group_save_checkpoint(pg_group* g, int label_idx, const char* path);
+int pg_group_load_checkpoint(pg_group* g, int label_idx, const char* path);
 int pg_group_mixture_sample(pg_group* g, const double* priors, long n, uint64_t seed, float* out, int* ids);
 /* device time (ms, CUDA events) of the last pg_group_train_steps call */
 float pg_group_last_ms(pg_group* g);

@@ -473,6 +473,12 @@ int pg_group_failed(pg_group* g, int* failed) {
   });
 }
 int pg_group_generate(pg_group* g, long n, uint64_t seed, float* out) { return WITH_GROUP(grp.generate(n, seed, out)); }
+int pg_group_save_checkpoint(pg_group* g, int label_idx, const char* path) {
+  return WITH_GROUP(pg::save_checkpoint(grp, label_idx, path));
+}
+int pg_group_load_checkpoint(pg_group* g, int label_idx, const char* path) {
+  return WITH_GROUP(pg::load_checkpoint(grp, label_idx, path));
+}
 int pg_group_mixture_sample(pg_group* g, const double* priors, long n, uint64_t seed, float* out, int* ids) {
   return WITH_GROUP(grp.mixture_sample(priors, n, seed, out, ids));
 }

@@ -438,6 +438,19 @@ void GanGroup::set(int label, int what, const double* in, long n) {
     case D_PARAMS: put(*D_, D_->params, false); return;
     case G_BUFFERS: put(*G_, G_->running, true); return;
     case D_BUFFERS: put(*D_, D_->running, true); return;
+    case G_M: put(*G_, G_->adam_m, false); return;
+    case G_V: put(*G_, G_->adam_v, false); return;
+    case D_M: put(*D_, D_->adam_m, false); return;
+    case D_V: put(*D_, D_->adam_v, false); return;
+    case COUNTERS: {
+      // Adam step counters of this label; the step count is group-wide (labels advance in lockstep)
+      if (n != 3) throw std::invalid_argument("length mismatch on set");
+      const long long tg = static_cast<long long>(in[0]), td = static_cast<long long>(in[1]);
+      check_cuda(cudaMemcpy(d_t_g_ + label, &tg, sizeof(tg), cudaMemcpyHostToDevice), "t");
+      check_cuda(cudaMemcpy(d_t_d_ + label, &td, sizeof(td), cudaMemcpyHostToDevice), "t");
+      steps_ = static_cast<long>(in[2]);
+      return;
+    }
   }
   throw std::invalid_argument("field not settable: " + std::to_string(what));
 }

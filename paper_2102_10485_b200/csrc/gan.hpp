@@ -122,4 +122,9 @@ class GanGroup {
   void drain_reports();
 };
 
+// checkpoint.cpp: one label's pair in the reference file format
+// (src/checkpoint.cpp:91-194 save_gan_pair / load_gan_pair)
+void save_checkpoint(GanGroup& grp, int label, const std::string& path);
+void load_checkpoint(GanGroup& grp, int label, const std::string& path);
+
 }  // namespace pg

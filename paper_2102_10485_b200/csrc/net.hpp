@@ -106,6 +106,7 @@ class DevNet {
   long ref_buffers() const { return ref_Bf_; }
   const std::vector<long>& ref_out_shape() const { return ref_shapes_.back(); }
   const std::vector<long>& ref_in_shape() const { return ref_shapes_.front(); }
+  const std::vector<LayerSpec>& layers() const { return layers_; }
   int math() const { return math_; }
   void set_math(int m) { math_ = m; }
 

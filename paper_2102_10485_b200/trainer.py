@@ -159,6 +159,14 @@ class LabelGroup:
         N.check(N.lib().pg_group_generate(self._h, n, seed, _fptr(out)), "generate")
         return out
 
+    def save_checkpoint(self, label: int, path: str) -> None:
+        """save_gan_pair (src/checkpoint.cpp:91-139) for label index `label`."""
+        N.check(N.lib().pg_group_save_checkpoint(self._h, label, str(path).encode()), "save_checkpoint")
+
+    def load_checkpoint(self, label: int, path: str) -> None:
+        """load_gan_pair (src/checkpoint.cpp:141-194) into label index `label`."""
+        N.check(N.lib().pg_group_load_checkpoint(self._h, label, str(path).encode()), "load_checkpoint")
+
     def mixture_sample(self, priors, n: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
         """mixture_sample (partition.cpp:182-227) over this group's labels in
         order: (samples [n][C][H][W] in [0,1], class indices [n])."""

@@ -297,3 +297,50 @@ def test_mixture_sample_matches_reference_protocol(oracle, math):
     rs, rids = one_o.mixture(np.array([1.0]), 50, 21, arch.image)
     assert np.all(ids == 0) and np.array_equal(ids, rids)
     assert np.abs(s - rs).max() <= 1e-4
+
+
+def test_checkpoint_roundtrip_in_reference_format(tmp_path):
+    """save_gan_pair / load_gan_pair (src/checkpoint.cpp:91-194): u32 LE header
+    length, a JSON header in the reference schema (blob table in the fixed
+    order, conv_transpose2d layers), f64 blobs; loading restores every field
+    bit for bit (params, buffers, Adam moments and step counters), and the
+    reference's error messages for foreign / truncated / mismatched files."""
+    import json
+    import struct
+    arch, grp = make_pair(1, 2, 128, 64, 1)
+    grp.train_steps(2)
+    path = tmp_path / "class_1.bin"
+    grp.save_checkpoint(1, str(path))
+    raw = path.read_bytes()
+    (hlen,) = struct.unpack("<I", raw[:4])
+    head = json.loads(raw[4:4 + hlen])
+    assert head["format"] == "partgan-checkpoint" and head["version"] == 1 and head["d_z"] == arch.d_z
+    assert [b["name"] for b in head["blobs"]] == ["gen_params", "gen_buffers", "disc_params", "disc_buffers",
+                                                  "opt_g_m", "opt_g_v", "opt_d_m", "opt_d_v"]
+    assert any(l["type"] == "conv_transpose2d" for l in head["generator"]["layers"])
+    assert head["opt_g"]["t"] == 2 and head["steps"] == 2
+    total = sum(b["len"] for b in head["blobs"])
+    assert len(raw) == 4 + hlen + 8 * total
+    blob0 = np.frombuffer(raw[4 + hlen:4 + hlen + 8 * head["blobs"][0]["len"]], "<f8")
+    assert np.array_equal(blob0, grp.get(1, N.F_GEN_PARAMS))
+
+    fresh = LabelGroup(GroupSpec(arch=arch, class_ids=[5], batch=64, per_label=128, base_seed=99, math=1))
+    fresh.load_checkpoint(0, str(path))
+    for code in (N.F_GEN_PARAMS, N.F_DISC_PARAMS, N.F_GEN_BUFFERS, N.F_DISC_BUFFERS, N.F_GEN_ADAM_M,
+                 N.F_GEN_ADAM_V, N.F_DISC_ADAM_M, N.F_DISC_ADAM_V, N.F_COUNTERS):
+        assert np.array_equal(fresh.get(0, code), grp.get(1, code)), code
+
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(struct.pack("<I", 7) + b'{"x": 1}')
+    with pytest.raises(Exception, match="not a checkpoint file"):
+        fresh.load_checkpoint(0, str(bad))
+    short = tmp_path / "short.bin"
+    short.write_bytes(raw[:4 + hlen + 100])
+    with pytest.raises(Exception, match="truncated blob 'gen_params'"):
+        fresh.load_checkpoint(0, str(short))
+    head["blobs"][2]["len"] += 1
+    h2 = json.dumps(head).encode()
+    lied = tmp_path / "lied.bin"
+    lied.write_bytes(struct.pack("<I", len(h2)) + h2 + raw[4 + hlen:])
+    with pytest.raises(Exception, match="blob 'disc_params' .* has length"):
+        fresh.load_checkpoint(0, str(lied))
