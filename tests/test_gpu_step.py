@@ -344,3 +344,36 @@ def test_checkpoint_roundtrip_in_reference_format(tmp_path):
     lied.write_bytes(struct.pack("<I", len(h2)) + h2 + raw[4 + hlen:])
     with pytest.raises(Exception, match="blob 'disc_params' .* has length"):
         fresh.load_checkpoint(0, str(lied))
+
+
+def test_cli_train_and_sample_artifacts(tmp_path):
+    """The reference driver's artifacts (run.cpp:363-444, test_cli.cpp:91-120,
+    180-195): one checkpoint per class, losses.csv with one row per step,
+    manifest.json; two runs with the same seed write byte-identical
+    checkpoints and losses; `sample` draws a mixture over the checkpoints."""
+    import json
+    import subprocess
+    import sys
+    outs = []
+    for run in ("a", "b"):
+        out = tmp_path / run
+        r = subprocess.run([sys.executable, "-m", "paper_2102_10485_b200", "train", "--arch", "1", "--labels", "3",
+                            "--per-label", "128", "--batch", "64", "--seed", "5", "--out", str(out)],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        outs.append(out)
+    a, b = outs
+    for k in range(3):
+        assert (a / f"checkpoints/class_{k}.bin").read_bytes() == (b / f"checkpoints/class_{k}.bin").read_bytes()
+    lines = (a / "losses.csv").read_text().splitlines()
+    assert lines[0] == "mode,class_id,step,j_d,j_g,d_real_mean,d_fake_mean" and len(lines) == 1 + 3 * 2
+    assert (a / "losses.csv").read_text() == (b / "losses.csv").read_text()
+    man = json.loads((a / "manifest.json").read_text())
+    assert man["format"] == "partgan-manifest" and man["k"] == 3 and len(man["workers"]) == 3
+    assert [w["checkpoint"] for w in man["workers"]] == [f"checkpoints/class_{k}.bin" for k in range(3)]
+    r = subprocess.run([sys.executable, "-m", "paper_2102_10485_b200", "sample", "--manifest", str(a / "manifest.json"),
+                        "--n", "40", "--out", str(tmp_path / "s.npz")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    z = np.load(tmp_path / "s.npz")
+    assert z["samples"].shape == (40, 1, 28, 28) and set(np.unique(z["class_ids"])) <= {0, 1, 2}
+    assert z["samples"].min() >= 0.0 and z["samples"].max() <= 1.0
