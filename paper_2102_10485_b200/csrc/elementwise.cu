@@ -13,15 +13,25 @@ namespace pg {
 
 namespace {
 
-constexpr int RED_ROWS = 512;  // rows per reduction chunk
 constexpr int RED_NT = 256;
+
+// rows per reduction chunk: 512, halved (down to 32) until the grid has ~8
+// blocks per SM, so the small deep-layer maps (a few hundred rows per label)
+// are not latency bound on a handful of blocks.  A pure function of the map:
+// the reduce kernel and every reader of its partials agree on it.
+__host__ __device__ inline int red_rows(const ChannelMap& cm) {
+  const int c4n = cm.Cp / 4, gpb = c4n < RED_NT ? c4n : RED_NT, ny = (c4n + gpb - 1) / gpb;
+  int rows = 512;
+  while (rows > 32 && (long long)cm.L * ny * ((cm.R + rows - 1) / rows) < 148 * 8) rows >>= 1;
+  return rows;
+}
 
 PG_DEV float4 f4(float v) { return make_float4(v, v, v, v); }
 PG_DEV float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
 PG_DEV float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
 // Per-channel sums over the rows of [L][R][Cp] maps.  Block = (label, chunk of
-// RED_ROWS rows, up to 256 float4 channel groups): a thread owns 4 channels
+// red_rows(cm) rows, up to 256 float4 channel groups): a thread owns 4 channels
 // (float4 loads along the row) and a row lane; the row lanes are combined in
 // shared memory in a fixed order, and the chunk partials by the finalize
 // kernels in chunk order (deterministic, no atomics).
@@ -29,7 +39,7 @@ __global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, i
                                                                 const float* __restrict__ gy,
                                                                 const float* __restrict__ y,
                                                                 const float* __restrict__ mean, int act, float slope,
-                                                                float* __restrict__ partial) {
+                                                                float* __restrict__ partial, float* __restrict__ g_out) {
   const int l = blockIdx.z, chunk = blockIdx.x, nchunk = gridDim.x;
   const int c4n = cm.Cp / 4;
   const int gpb = c4n < RED_NT ? c4n : RED_NT;  // channel groups per block
@@ -40,9 +50,10 @@ __global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, i
   if (g < c4n && lr < lanes) {
     const float4 mu = (mode == RED_SQDEV || mode == RED_BN_BWD) ? ld4(mean + (long long)l * cm.Cp + 4 * g) : f4(0.f);
     const long long base = (long long)l * cm.ls + 4 * g;
-    const int r_end = min(cm.R, (chunk + 1) * RED_ROWS);
+    const int rows = red_rows(cm);
+    const int r_end = min(cm.R, (chunk + 1) * rows);
 #pragma unroll 4
-    for (int r = chunk * RED_ROWS + lr; r < r_end; r += lanes) {
+    for (int r = chunk * rows + lr; r < r_end; r += lanes) {
       const long long o = base + (long long)r * cm.Cp;
       if (mode == RED_SUM) {
         s0 = add4(s0, ld4(x + o));
@@ -55,6 +66,7 @@ __global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, i
         const float4 g1 = make_float4(act_bwd(act, g4.x, y4.x, slope), act_bwd(act, g4.y, y4.y, slope),
                                       act_bwd(act, g4.z, y4.z, slope), act_bwd(act, g4.w, y4.w, slope));
         s0 = add4(s0, g1);
+        if (g_out) *reinterpret_cast<float4*>(g_out + o) = g1;  // RED_ACT_G: the activation backward itself
         if (mode == RED_BN_BWD) {
           const float4 v = ld4(x + o);
           const float4 d = make_float4(v.x - mu.x, v.y - mu.y, v.z - mu.z, v.w - mu.w);
@@ -80,7 +92,7 @@ __global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, i
 }
 
 PG_DEV float sum_partials(const ChannelMap& cm, const float* partial, int l, int k, int c) {
-  const int nchunk = cm.nslot > 0 ? cm.nslot : (cm.R + RED_ROWS - 1) / RED_ROWS;
+  const int nchunk = cm.nslot > 0 ? cm.nslot : (cm.R + red_rows(cm) - 1) / red_rows(cm);
   const int pk = cm.nslot > 0 ? 4 : 3;
   float t = 0.f;
   for (int ch = 0; ch < nchunk; ++ch) t += partial[(((long long)l * nchunk + ch) * pk + k) * cm.Cp + c];
@@ -527,15 +539,18 @@ unsigned grid_for(long long work, int per_block, unsigned cap = 148 * 16) {
 
 }  // namespace
 
-int reduce_chunks(int R) { return (R + RED_ROWS - 1) / RED_ROWS; }
-size_t reduce_partial_floats(const ChannelMap& cm) { return (size_t)cm.L * reduce_chunks(cm.R) * 3 * cm.Cp; }
+int reduce_chunks(const ChannelMap& cm) { return (cm.R + red_rows(cm) - 1) / red_rows(cm); }
+// sized for the smallest chunk, so any map with at most cm.R rows fits
+size_t reduce_partial_floats(const ChannelMap& cm) { return (size_t)cm.L * ((cm.R + 31) / 32) * 3 * cm.Cp; }
 
 cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x, const float* gy, const float* y,
-                                  const float* mean, int act, float slope, float* partial, cudaStream_t st) {
+                                  const float* mean, int act, float slope, float* partial, cudaStream_t st,
+                                  float* g_out) {
   if (cm.Cp % 4) return cudaErrorInvalidValue;
   const int c4n = cm.Cp / 4, gpb = c4n < RED_NT ? c4n : RED_NT;
-  dim3 grid(reduce_chunks(cm.R), (c4n + gpb - 1) / gpb, cm.L);
-  channel_reduce_kernel<<<grid, RED_NT, 0, st>>>(cm, mode, x, gy, y, mean, act, slope, partial);
+  dim3 grid(reduce_chunks(cm), (c4n + gpb - 1) / gpb, cm.L);
+  channel_reduce_kernel<<<grid, RED_NT, 0, st>>>(cm, mode, x, gy, y, mean, act, slope, partial,
+                                                  mode == RED_ACT_G ? g_out : nullptr);
   return launched();
 }
 

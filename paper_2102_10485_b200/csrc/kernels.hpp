@@ -61,11 +61,13 @@ struct ChannelMap {
   int nslot = 0;
   int npack = 1;  // statistic columns per channel (see gemm_stat_slots)
 };
-int reduce_chunks(int R);
+int reduce_chunks(const ChannelMap& cm);
 size_t reduce_partial_floats(const ChannelMap& cm);
 // partial: [L][chunks][3][Cp]
+// RED_ACT_G with g_out: also writes g1 = act_bwd(gy, y) (activation backward + bias sums in one pass)
 cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x, const float* gy, const float* y,
-                                  const float* mean, int act, float slope, float* partial, cudaStream_t st);
+                                  const float* mean, int act, float slope, float* partial, cudaStream_t st,
+                                  float* g_out = nullptr);
 
 // BN forward finalize: pass 0 -> mean; pass 1 -> var, inv_std, running-stat update.
 cudaError_t launch_bn_finalize_mean(const ChannelMap& cm, const float* partial, float* mean, cudaStream_t st);

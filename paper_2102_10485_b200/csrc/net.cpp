@@ -594,7 +594,16 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
                  "bn bwd apply");
       gz = gz_.p;
     } else if (b.act != ACT_NONE && !fused) {
-      check_cuda(launch_act_bwd(cm, gy, t.act[i + 1], b.act, b.slope, gz_.p, st), "act bwd");
+      if (param_grads) {
+        // activation backward and the bias sums in one pass over (gy, y)
+        check_cuda(launch_channel_reduce(cm, RED_ACT_G, nullptr, gy, t.act[i + 1], nullptr, b.act, b.slope, partial_.p,
+                                         st, gz_.p),
+                   "act bwd + bias reduce");
+        check_cuda(launch_bias_finalize(cm, partial_.p, dbias, P_, accumulate ? 1 : 0, st), "bias finalize");
+        bias_done = true;
+      } else {
+        check_cuda(launch_act_bwd(cm, gy, t.act[i + 1], b.act, b.slope, gz_.p, st), "act bwd");
+      }
       gz = gz_.p;
     }
     if (param_grads && !bias_done && fused && !b.has_bn) {

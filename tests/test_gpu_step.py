@@ -156,7 +156,7 @@ def test_single_step_parity(oracle, cfg, n_labels, per_label, batch, math):
         assert abs(r[2] - q[2]) <= 1e-4 * abs(q[2]), (r, q)   # mean D(real)
         assert abs(r[3] - q[3]) <= 1e-4 * abs(q[3]), (r, q)   # mean D(fake)
         assert abs(r[1] - q[1]) <= 1e-3 * abs(q[1]), (r, q)   # J_G, after the D update
-    compare_grads(grp, orc, arch, n_labels, nets=("D",), l2_only=KINK_L2 if math else None)
+    compare_grads(grp, orc, arch, n_labels, nets=("D",), l2_only=KINK_L2_CFG.get(cfg, KINK_L2))
     compare_params_after_update(grp, orc, arch, n_labels)
     assert not grp.failed().any()
 
