@@ -44,6 +44,8 @@ GanGroup::GanGroup(const GroupConfig& cfg) : cfg_(cfg), L_(static_cast<int>(cfg.
   if (dout != 1) throw std::invalid_argument("discriminator must emit a scalar");
 
   check_cuda(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+  check_cuda(cudaStreamCreateWithFlags(&cst_, cudaStreamNonBlocking), "copy stream");
+  check_cuda(cudaEventCreateWithFlags(&real_ready_, cudaEventDisableTiming), "event");
   tg_ = G_->make_trace(true);
   tdr_ = D_->make_trace(true);
   tdf_ = D_->make_trace(true);
@@ -104,6 +106,11 @@ GanGroup::GanGroup(const GroupConfig& cfg) : cfg_(cfg), L_(static_cast<int>(cfg.
 
 GanGroup::~GanGroup() {
   if (st_) cudaStreamSynchronize(st_);
+  if (cst_) {
+    cudaStreamSynchronize(cst_);
+    cudaStreamDestroy(cst_);
+  }
+  if (real_ready_) cudaEventDestroy(real_ready_);
   for (int par = 0; par < 2; ++par) {
     cudaFree(d_idx_[par]);
     cudaFreeHost(h_idx_[par]);
@@ -194,7 +201,7 @@ void GanGroup::prep_host(int par, int B, bool with_idx) {
 }
 
 // The adversarial step (gan.cpp:136-176) for all labels, on st_.
-void GanGroup::enqueue_step(int B, const float* real_nhwc, int par) {
+void GanGroup::enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t real_ready) {
   const int pstride = static_cast<int>(D_->out_map().Cp);
   const int nbg = G_->blocks(), nbd = D_->blocks();
   double* rep = d_rep_ + (steps_ % rep_cap_) * L_ * 4;
@@ -202,6 +209,7 @@ void GanGroup::enqueue_step(int B, const float* real_nhwc, int par) {
   tg_.act[0] = dz_[par][0].p;
   G_->forward(tg_, B, true, true, st_);
   tdr_.act[0] = const_cast<float*>(real_nhwc);
+  if (real_ready) check_cuda(cudaStreamWaitEvent(st_, real_ready, 0), "wait real batch");
   D_->forward(tdr_, B, true, true, st_);
   tdf_.act[0] = tg_.act[static_cast<size_t>(nbg)];
   D_->forward(tdf_, B, true, true, st_);
@@ -280,6 +288,21 @@ int GanGroup::train_steps(int n) {
   return done;
 }
 
+// The host real batch goes up on the copy stream while the generator's forward
+// (which only needs z1) runs: H2D into the gradient scratch (same extent, idle
+// until the generator step), NCHW -> NHWC with 2x-1, then real_ready_, which
+// the discriminator's forward on the real batch waits for.  Callers end every
+// step with a stream sync, so both buffers are free here.
+void GanGroup::stage_real_async(const float* real01, int B) {
+  const Map& im = D_->in_map();
+  const size_t rb = sizeof(float) * static_cast<size_t>(L_) * B * cfg_.C * cfg_.H * cfg_.W;
+  check_cuda(cudaMemcpyAsync(gimg_.p, real01, rb, cudaMemcpyHostToDevice, cst_), "real H2D");
+  check_cuda(launch_nchw01_to_nhwc(static_cast<long long>(L_) * B, static_cast<int>(cfg_.C), static_cast<int>(cfg_.H),
+                                   static_cast<int>(cfg_.W), static_cast<int>(im.Cp), gimg_.p, real_.p, cst_),
+             "real layout");
+  check_cuda(cudaEventRecord(real_ready_, cst_), "event");
+}
+
 void GanGroup::train_step_host(const float* real01, int B, double* reports) {
   if (B < 1 || B > std::min<long>(cfg_.batch, cfg_.per_label)) throw std::invalid_argument("train_step: batch size out of range");
   const Map& im = D_->in_map();
@@ -291,14 +314,9 @@ void GanGroup::train_step_host(const float* real01, int B, double* reports) {
   check_cuda(cudaMemcpyAsync(dz_[par][1].p, h_z_[par] + static_cast<size_t>(L_) * B * zcp_, zb, cudaMemcpyHostToDevice,
                              st_),
              "z2 H2D");
-  // real batch H2D into the gradient scratch (same extent), then NCHW->NHWC with 2x-1
-  const size_t rb = sizeof(float) * static_cast<size_t>(L_) * B * cfg_.C * cfg_.H * cfg_.W;
-  check_cuda(cudaMemcpyAsync(gimg_.p, real01, rb, cudaMemcpyHostToDevice, st_), "real H2D");
   check_cuda(cudaEventRecord(staged_[par], st_), "event");
-  check_cuda(launch_nchw01_to_nhwc(static_cast<long long>(L_) * B, static_cast<int>(cfg_.C), static_cast<int>(cfg_.H),
-                                   static_cast<int>(cfg_.W), static_cast<int>(im.Cp), gimg_.p, real_.p, st_),
-             "real layout");
-  enqueue_step(B, real_.p, par);
+  stage_real_async(real01, B);
+  enqueue_step(B, real_.p, par, real_ready_);
   drain_reports();
   if (reports)
     for (int l = 0; l < L_; ++l) {
@@ -326,13 +344,9 @@ void GanGroup::train_step_inputs(const float* real01, const float* z1, const flo
   check_cuda(cudaMemcpyAsync(dz_[par][0].p, hz, zb, cudaMemcpyHostToDevice, st_), "z1 H2D");
   check_cuda(cudaMemcpyAsync(dz_[par][1].p, hz + static_cast<size_t>(L_) * B * zcp_, zb, cudaMemcpyHostToDevice, st_),
              "z2 H2D");
-  const size_t rb = sizeof(float) * static_cast<size_t>(L_) * B * cfg_.C * cfg_.H * cfg_.W;
-  check_cuda(cudaMemcpyAsync(gimg_.p, real01, rb, cudaMemcpyHostToDevice, st_), "real H2D");
   check_cuda(cudaEventRecord(staged_[par], st_), "event");
-  check_cuda(launch_nchw01_to_nhwc(static_cast<long long>(L_) * B, static_cast<int>(cfg_.C), static_cast<int>(cfg_.H),
-                                   static_cast<int>(cfg_.W), static_cast<int>(im.Cp), gimg_.p, real_.p, st_),
-             "real layout");
-  enqueue_step(B, real_.p, par);
+  stage_real_async(real01, B);
+  enqueue_step(B, real_.p, par, real_ready_);
   drain_reports();
   if (reports)
     for (int l = 0; l < L_; ++l) {

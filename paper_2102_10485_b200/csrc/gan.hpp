@@ -90,6 +90,8 @@ class GanGroup {
   std::unique_ptr<DevNet> G_, D_;
   Trace tg_, tdr_, tdf_;
   cudaStream_t st_ = nullptr;
+  cudaStream_t cst_ = nullptr;      // host batch uploads, overlapped with the generator's forward
+  cudaEvent_t real_ready_ = nullptr;
   DeviceBuf data_, dz_[2][2], real_, gp_real_, gp_fake_, gimg_;
   int* d_idx_[2] = {nullptr, nullptr};
   int* d_flags_ = nullptr;
@@ -118,7 +120,8 @@ class GanGroup {
 
   int next_batch_size() const;
   void prep_host(int par, int B, bool with_idx);
-  void enqueue_step(int B, const float* real_nhwc, int par);
+  void enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t real_ready = nullptr);
+  void stage_real_async(const float* real01, int B);
   void drain_reports();
 };
 
