@@ -152,10 +152,16 @@ def run_reference(args) -> None:
         "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * sum(times) / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (cosine fields)",
-        "config": {"workload": f"c{args.cfg} architecture, {cores} labels per step sample, per-label batch "
-                               f"{args.batch}", "arch": baseline_arch(args.cfg).name},
+        # the same workload as our arm's line; the CPU times a bounded sample of it per step
+        "config": {"workload": f"c{args.cfg} arch sweep: {args.labels_per_gpu} labels/GPU, per-label batch "
+                               f"{args.batch}, {'x'.join(map(str, baseline_arch(args.cfg).image))}",
+                   "labels_per_gpu": args.labels_per_gpu, "global_batch": args.gpus * args.labels_per_gpu * args.batch,
+                   "per_label": args.per_label, "math": "f64 (reference CPU algorithm)",
+                   "parallelism": f"one worker thread per label, {cores} host threads"},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": f"{cores} labels x 1 step x batch {args.batch} per timed step"},
+                         "sample": f"{cores} labels x 1 step x batch {args.batch} per timed step (of the "
+                                   f"{args.labels_per_gpu} labels/GPU workload; the f64 oracle port of the "
+                                   f"reference per-sample im2col+GEMM path, one worker thread per label)"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
