@@ -646,13 +646,18 @@ constexpr int ATM_SA = 4;
 constexpr int ATM_ACOL = 256;
 __host__ __device__ constexpr int atm_bufs(int bn) { return 256 / bn; }
 __host__ __device__ constexpr int atm_lo_bytes(int bn) { return (bn / 2) * BKT * 4; }
+// split slot = a copy of the B half (hi) + its lo part: the MMA reads only
+// TMEM (A) and the split slots (B), so a TMA stage is released as soon as the
+// split warps have read it, not when the MMAs retire -- the TMA ring stays in
+// flight (the single-stage-in-flight ring was the feed limit of these tiles)
+__host__ __device__ constexpr int atm_slot_bytes(int bn) { return 2 * atm_lo_bytes(bn); }
 __host__ __device__ constexpr int atm_hi_stages(int bn) {
-  return (SMEM_BUDGET - ATM_SA * atm_lo_bytes(bn)) / stage_bytes(bn) > 8
+  return (SMEM_BUDGET - ATM_SA * atm_slot_bytes(bn)) / stage_bytes(bn) > 8
              ? 8
-             : (SMEM_BUDGET - ATM_SA * atm_lo_bytes(bn)) / stage_bytes(bn);
+             : (SMEM_BUDGET - ATM_SA * atm_slot_bytes(bn)) / stage_bytes(bn);
 }
 __host__ __device__ constexpr int atm_smem(int bn) {
-  return atm_hi_stages(bn) * stage_bytes(bn) + ATM_SA * atm_lo_bytes(bn) + 1024 + 1024;
+  return atm_hi_stages(bn) * stage_bytes(bn) + ATM_SA * atm_slot_bytes(bn) + 1024 + 1024;
 }
 
 template <int KIND, int BN, bool STATS>
@@ -672,7 +677,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* lo_base = smem + SH * SB;
-  uint64_t* full_h = reinterpret_cast<uint64_t*>(lo_base + ATM_SA * LB);
+  uint64_t* full_h = reinterpret_cast<uint64_t*>(lo_base + ATM_SA * 2 * LB);
   uint64_t* empty_h = full_h + SH;
   uint64_t* ready = empty_h + SH;
   uint64_t* empty_l = ready + ATM_SA;
@@ -688,7 +693,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
   if (tid == 0) {
     for (int s = 0; s < SH; ++s) {
       mbar_init(full_h + s, 1);
-      mbar_init(empty_h + s, 1);
+      mbar_init(empty_h + s, 4);  // released by the four split warps of this CTA
     }
     for (int s = 0; s < ATM_SA; ++s) {
       mbar_init(ready + s, 2 * 4);
@@ -735,13 +740,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
         tmem_st32(ta, hi);
         tmem_st32(ta + 32, lo);
         const float4* bsrc = reinterpret_cast<const float4*>(smem + s * SB + AB);
-        float4* bdst = reinterpret_cast<float4*>(lo_base + j * LB);
+        float4* bhi = reinterpret_cast<float4*>(lo_base + j * 2 * LB);
+        float4* blo = reinterpret_cast<float4*>(lo_base + j * 2 * LB + LB);
 #pragma unroll
         for (int e = tid; e < LB / 16; e += 128) {
           const float4 v = bsrc[e];
-          bdst[e] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
-                                v.w - tf32_trunc(v.w));
+          bhi[e] = v;
+          blo[e] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                               v.w - tf32_trunc(v.w));
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_h + s);  // the TMA stage is fully read: refill it now
         tmem_st_wait();
         fence_async_smem();
         tc_fence_before();
@@ -793,8 +802,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
             mbar_wait_cluster(ready + j, (it / ATM_SA) & 1);
             tc_fence_after();
             const uint32_t a_t = tmem + ATM_ACOL + j * 64;
-            const uint32_t b_hi = smem_u32(smem + s * SB) + AB;
-            const uint32_t b_lo = smem_u32(lo_base + j * LB);
+            const uint32_t b_hi = smem_u32(lo_base + j * 2 * LB);
+            const uint32_t b_lo = b_hi + LB;
 #pragma unroll
             for (int kk = 0; kk < BKT / 8; ++kk) {
               const uint64_t bh = make_desc(b_hi + kk * b_step, b_lbo, b_sbo, b_lay);
@@ -804,7 +813,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
               mma_tf32_pair_ts(dacc, a_t + kk * 8, bl, idesc, 1u);
               mma_tf32_pair_ts(dacc, a_t + kk * 8, bh, idesc, 1u);
             }
-            mma_commit_pair(empty_h + s, 3);
             mma_commit_pair(empty_l + j, 3);
           }
           mma_commit_pair(seg_full + buf, 3);
