@@ -42,10 +42,16 @@ using namespace tmac;
 
 constexpr int BM = 128;   // rows per CTA
 constexpr int BKT = 32;   // fp32 of K per k-block (one 128-byte row)
-constexpr int NSPLIT = 2; // split / forward warps
+// split / forward warps: the lo split of a k-block must keep up with its MMAs,
+// which take half as long on BN <= 128 tiles (measured: 2 warps paced the
+// narrow tiles in TF32X3 once MMA issue was warp-uniform)
+// (FPROP / DGRAD in TF32X3; the WGRAD tiles measured slower with 4: 1.45 vs 1.35 ms)
+__host__ __device__ constexpr int nsplit(int kind, int bn, int mode) {
+  return bn <= 128 && kind != GEMM_WGRAD && mode == MATH_TF32X3 ? 4 : 2;
+}
+__host__ __device__ constexpr int pair_nt(int kind, int bn, int mode) { return (nsplit(kind, bn, mode) + 2 + 8) * 32; }
 constexpr int NDRAIN = 8;
-constexpr int NT = (4 + NDRAIN) * 32;
-constexpr int W_MMA = 3, W_DRAIN = 4;
+constexpr int W_DRAIN = 4;  // first drain warp of the A-in-TMEM kernel
 constexpr int SMEM_BUDGET = 200 * 1024;
 constexpr int KIND_DGP = 3;  // phase-packed stride-2 DGRAD (k = 4, s = 2, p = 1), engine-internal
 // widest packed N: packing CG = 128 (N = 512) measured 1.36 vs 1.22 ms on the
@@ -369,12 +375,11 @@ PG_DEV void pair_issue(const CUtensorMap& tmA, const CUtensorMap& tmB, const Pai
 // writes the tile (epi_store / epi_stats)
 template <int KIND, int BN, bool STATS, int NB>
 PG_DEV void pair_drain_role(const PairPlan& P, uint32_t tmem, uint64_t* seg_full, uint64_t* seg_empty, int dw,
-                            int lane, uint32_t rank, int cl, int ncl, int ntiles) {
+                            int warp, int lane, uint32_t rank, int cl, int ncl, int ntiles) {
   constexpr int BH = BN / 2;
   const ConvGeo& g = P.g;
-  const int warp = dw + W_DRAIN;
     const int q = warp & 3;               // TMEM lane quarter
-    const int half = (warp - W_DRAIN) >> 2;  // accumulator column half
+    const int half = dw >> 2;  // accumulator column half (drain warp index dw = 0..7)
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const uint32_t seg_empty_leader = mapa_shared(smem_u32(seg_empty), 0);
     uint32_t sc = 0;
@@ -461,7 +466,7 @@ PG_DEV void pair_drain_role(const PairPlan& P, uint32_t tmem, uint64_t* seg_full
   }
 
 template <int KIND, int BN, int MODE, bool STATS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MODE), 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const PairPlan P) {
   constexpr bool SPLIT = MODE == MATH_TF32X3;
@@ -475,6 +480,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
   constexpr bool B_MN = KIND != GEMM_FPROP && KIND != KIND_F4;  // DGRAD / KIND_DGP weights, WGRAD gradients: N-major
   constexpr int NB = seg_bufs(BN);
   constexpr uint32_t TMEM_COLS = NB * BN;
+  constexpr int NSPLIT = nsplit(KIND, BN, MODE);
+  constexpr int W_MMA = NSPLIT + 1, W_DR = NSPLIT + 2;  // warp 0 TMA, 1..NSPLIT split, MMA, 8 drain warps
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -567,7 +574,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
     }
   } else if (warp == W_MMA) {
     // ===================== MMA issuer (leader CTA only) =====================
-    if (rank == 0 && lane == 0) {
+    // The whole warp runs the loop (warp-uniform values stay in uniform
+    // registers); one elected lane issues the MMAs and the commits.  With a
+    // divergent single-lane loop every MMA paid ~12 instructions of R2UR /
+    // ELECT re-materialisation, which paced the narrow (N <= 128) tiles.
+    if (rank == 0) {
       constexpr uint32_t idesc = make_idesc(2 * BM, BN, A_MN, B_MN);
       // K-major SW128: 8-row atoms at 1024 B, K-step of 8 fp32 = +32 B inside the row.
       // MN-major SW128_BASE32B: 4-row atoms at 512 B along K, 32-wide MN atoms at 4096 B.
@@ -577,6 +588,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
       constexpr uint32_t b_lbo = B_MN ? 4096u : 16u, b_sbo = B_MN ? 512u : 1024u, b_step = B_MN ? 1024u : 32u;
       constexpr uint32_t a_lay = A_MN ? UMMA_SW128_BASE32B : F4 ? UMMA_SW_NONE : UMMA_SW128;
       constexpr uint32_t b_lay = B_MN ? UMMA_SW128_BASE32B : UMMA_SW128;
+      // descriptors are linear in the start address (bits 0-13 = addr >> 4)
+      const uint64_t a_desc0 = make_desc(smem_u32(smem), a_lbo, a_sbo, a_lay);
+      const uint64_t b_desc0 = make_desc(smem_u32(smem) + AB, b_lbo, b_sbo, b_lay);
+      const uint64_t al_desc0 = make_desc(smem_u32(lo_base), a_lbo, a_sbo, a_lay);
+      const uint64_t bl_desc0 = make_desc(smem_u32(lo_base) + AB, b_lbo, b_sbo, b_lay);
       uint32_t it = 0, sc = 0;
       for (int t = cl; t < ntiles; t += ncl) {
         for (int k_seg = 0; k_seg < P.nk; k_seg += P.kseg, ++sc) {
@@ -590,33 +606,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1)
             const int j = SPLIT ? it % SL : 0;
             mbar_wait_cluster(ready + (SPLIT ? j : s), (it / RS) & 1);
             tc_fence_after();
-            const uint32_t a_hi = smem_u32(smem + s * SB), b_hi = a_hi + AB;
-            const uint32_t a_lo = smem_u32(lo_base + j * SB), b_lo = a_lo + AB;
+            const uint64_t ah0 = a_desc0 + (uint64_t)((s * SB) >> 4), bh0 = b_desc0 + (uint64_t)((s * SB) >> 4);
+            const uint64_t al0 = al_desc0 + (uint64_t)((j * SB) >> 4), bl0 = bl_desc0 + (uint64_t)((j * SB) >> 4);
+            if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < BKT / 8; ++kk) {
-              const uint64_t ah = make_desc(a_hi + kk * a_step, a_lbo, a_sbo, a_lay);
-              const uint64_t bh = make_desc(b_hi + kk * b_step, b_lbo, b_sbo, b_lay);
-              const uint32_t acc = (kb != k_seg || kk) ? 1u : 0u;
-              if (SPLIT) {
-                const uint64_t al = make_desc(a_lo + kk * a_step, a_lbo, a_sbo, a_lay);
-                const uint64_t bl = make_desc(b_lo + kk * b_step, b_lbo, b_sbo, b_lay);
-                mma_tf32_pair(d, al, bh, idesc, acc);  // small terms first
-                mma_tf32_pair(d, ah, bl, idesc, 1u);
-                mma_tf32_pair(d, ah, bh, idesc, 1u);
-              } else {
-                mma_tf32_pair(d, ah, bh, idesc, acc);
+              for (int kk = 0; kk < BKT / 8; ++kk) {
+                const uint64_t ah = ah0 + (kk * a_step >> 4), bh = bh0 + (kk * b_step >> 4);
+                const uint32_t acc = (kb != k_seg || kk) ? 1u : 0u;
+                if (SPLIT) {
+                  mma_tf32_pair(d, al0 + (kk * a_step >> 4), bh, idesc, acc);  // small terms first
+                  mma_tf32_pair(d, ah, bl0 + (kk * b_step >> 4), idesc, 1u);
+                  mma_tf32_pair(d, ah, bh, idesc, 1u);
+                } else {
+                  mma_tf32_pair(d, ah, bh, idesc, acc);
+                }
               }
+              mma_commit_pair(empty_h + s, 3);
+              if (SPLIT) mma_commit_pair(empty_l + j, 3);
+              if (kb + 1 == k_end) mma_commit_pair(seg_full + buf, 3);
             }
-            mma_commit_pair(empty_h + s, 3);
-            if (SPLIT) mma_commit_pair(empty_l + j, 3);
+            __syncwarp();
           }
-          mma_commit_pair(seg_full + buf, 3);
         }
       }
     }
     __syncwarp();
   } else {
-    pair_drain_role<KIND, BN, STATS, NB>(P, tmem, seg_full, seg_empty, warp - W_DRAIN, lane, rank, cl, ncl, ntiles);
+    pair_drain_role<KIND, BN, STATS, NB>(P, tmem, seg_full, seg_empty, warp - W_DR, warp, lane, rank, cl, ncl,
+                                         ntiles);
   }
   tc_fence_before();
   __syncthreads();
@@ -759,7 +776,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
       }
     }
   } else if (warp < 4 + NDRAIN) {
-    pair_drain_role<KIND, BN, STATS, NB>(P, tmem, seg_full, seg_empty, warp - W_DRAIN, lane, rank, cl, ncl, ntiles);
+    pair_drain_role<KIND, BN, STATS, NB>(P, tmem, seg_full, seg_empty, warp - W_DRAIN, warp, lane, rank, cl, ncl,
+                                         ntiles);
   } else if (warp == W_TMA) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
@@ -843,7 +861,7 @@ cudaError_t launch_pair_st(const CUtensorMap& ta, const CUtensorMap& tb, const P
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gemm_pair_kernel<KIND, BN, MODE, STATS><<<grid, NT, smem, st>>>(ta, tb, P);
+  gemm_pair_kernel<KIND, BN, MODE, STATS><<<grid, pair_nt(KIND, BN, MODE), smem, st>>>(ta, tb, P);
   return launched();
 }
 

@@ -122,6 +122,15 @@ PG_DEV void tma_load_5d(uint32_t dst, const void* tmap, uint64_t* bar, int c0, i
       : "memory");
 }
 
+// one lane of the (fully active) warp: the lowest; the same lane every call
+PG_DEV bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- CTA pairs (cluster of 2, cta_group::2) --------------------------------
 PG_DEV uint32_t cluster_ctarank() {
   uint32_t r;
