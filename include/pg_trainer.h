@@ -91,6 +91,16 @@ int pg_group_sync(pg_group* g);
 int pg_group_sizes(pg_group* g, long long* out);
 
 /* Helpers shared with the reference protocol. */
+/* Evaluation of generated samples (host, f64; reference src/eval.cpp):
+ * softmax_rows (eval.cpp:18-33), inception_score (43-94: split_scores[n_splits],
+ * mean, stddev), anova_f over groups given as concatenated values + sizes[k]
+ * (158-186, +inf when the within-group variance is 0), anova_per_channel over
+ * images [n][C][H][W] with labels[n] (188-211, f[C]) */
+int pg_softmax_rows(const double* logits, long n, long k, double* probs);
+int pg_inception_score(const double* probs, long n, long k, int n_splits, double* split_scores, double* mean,
+                       double* stddev);
+int pg_anova_f(const double* values, const long* sizes, long k, double* f);
+int pg_anova_per_channel(const float* images, const int* labels, long n, long C, long H, long W, long k, double* f);
 uint64_t pg_derive_seed(uint64_t base, uint64_t stream_id);
 /* GPU g of n_gpus owns labels [pg_shard_begin(n, P, g), pg_shard_begin(n, P, g+1)) */
 int pg_shard_begin(int n_labels, int n_gpus, int g);

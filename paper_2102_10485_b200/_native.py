@@ -86,6 +86,12 @@ _SIGNATURES = {
     "pg_group_set": (C.c_int, [_P, C.c_int, C.c_int, _D, C.c_long]),
     "pg_group_failed": (C.c_int, [_P, _I]),
     "pg_group_generate": (C.c_int, [_P, C.c_long, C.c_uint64, _F]),
+    "pg_softmax_rows": (C.c_int, [C.POINTER(C.c_double), C.c_long, C.c_long, C.POINTER(C.c_double)]),
+    "pg_inception_score": (C.c_int, [C.POINTER(C.c_double), C.c_long, C.c_long, C.c_int, C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "pg_anova_f": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_long), C.c_long, C.POINTER(C.c_double)]),
+    "pg_anova_per_channel": (C.c_int, [_F, C.POINTER(C.c_int), C.c_long, C.c_long, C.c_long, C.c_long, C.c_long,
+                                       C.POINTER(C.c_double)]),
     "pg_group_save_checkpoint": (C.c_int, [_P, C.c_int, C.c_char_p]),
     "pg_group_load_checkpoint": (C.c_int, [_P, C.c_int, C.c_char_p]),
     "pg_group_mixture_sample": (C.c_int, [_P, C.POINTER(C.c_double), C.c_long, C.c_uint64, _F, C.POINTER(C.c_int)]),

@@ -5,6 +5,14 @@
 #include "../../include/pg_trainer.h"
 #include "gan.hpp"
 
+namespace pg {
+void softmax_rows(const double* logits, long n, long k, double* probs);
+void inception_score(const double* probs, long n, long k, int n_splits, double* split_scores, double* mean,
+                     double* stddev);
+double anova_f(const double* values, const long* sizes, long k);
+void anova_per_channel(const float* images, const int* labels, long n, long C, long H, long W, long k, double* f);
+}  // namespace pg
+
 namespace {
 
 thread_local std::string g_err;
@@ -491,6 +499,20 @@ int pg_group_sizes(pg_group* g, long long* out) {
     out[2] = grp.gen().P();
     out[3] = grp.disc().P();
   });
+}
+
+int pg_softmax_rows(const double* logits, long n, long k, double* probs) {
+  return guard([&] { pg::softmax_rows(logits, n, k, probs); });
+}
+int pg_inception_score(const double* probs, long n, long k, int n_splits, double* split_scores, double* mean,
+                       double* stddev) {
+  return guard([&] { pg::inception_score(probs, n, k, n_splits, split_scores, mean, stddev); });
+}
+int pg_anova_f(const double* values, const long* sizes, long k, double* f) {
+  return guard([&] { *f = pg::anova_f(values, sizes, k); });
+}
+int pg_anova_per_channel(const float* images, const int* labels, long n, long C, long H, long W, long k, double* f) {
+  return guard([&] { pg::anova_per_channel(images, labels, n, C, H, W, k, f); });
 }
 
 uint64_t pg_derive_seed(uint64_t base, uint64_t stream) { return pg::derive_seed(base, stream); }
