@@ -30,6 +30,14 @@ PG_DEV float4 f4(float v) { return make_float4(v, v, v, v); }
 PG_DEV float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
 PG_DEV float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
+// BN output before the activation, a = gamma * istd: ONE rounding point shared
+// by bn_apply and the backward kernels that recompute the activation output
+// from the pre-BN map (bit-identical to the y bn_apply wrote)
+PG_DEV float bn_pre(float a, float x, float m, float b) { return __fmaf_rn(a, x - m, b); }
+// the activation backward of a BN block can be taken from (x, BN coefficients)
+// instead of a stored y when the derivative depends on y only through its sign
+PG_DEV bool sign_act(int act) { return act == ACT_RELU || act == ACT_LRELU; }
+
 // Per-channel sums over the rows of [L][R][Cp] maps.  Block = (label, chunk of
 // red_rows(cm) rows, up to 256 float4 channel groups): a thread owns 4 channels
 // (float4 loads along the row) and a row lane; the row lanes are combined in
@@ -99,52 +107,79 @@ PG_DEV float sum_partials(const ChannelMap& cm, const float* partial, int l, int
   return t;
 }
 
-// Per-slot {shift, sum d, sum d^2, n} (d = z - shift) -> mean / M2 merged with
-// Chan's formula in f64; var is the biased variance over all rows
-// (network.cpp:171-184), running stats as bn_finalize_var.  Block = 32
-// channels x 8 slot lanes: lane j merges slots j, j+8, ... in order, then lane 0
-// merges the 8 lane results in order (deterministic, independent of timing).
-struct Moments {
-  double n, mu, m2;
+// Per-slot {shift, sum d, sum d^2, n} (d = z - shift) -> mean and biased
+// variance over all rows (network.cpp:171-184), running stats as
+// bn_finalize_var.  The slots are re-expressed against one per-channel
+// reference K (the first entry's shift, a value of the channel itself) and
+// summed in f64: with d' = shift - K,  S1 += sum_d + n d',  S2 += sum_d2 +
+// 2 d' sum_d + n d'^2  -- additions only (the per-slot Chan merge spent most of
+// the kernel in f64 divisions).  Block = 32 channels x nl lanes: lane j sums
+// the (slot, pack column) entries j, j + nl, ... in order, then a fixed
+// pairwise tree adds the lanes (deterministic, independent of timing).
+struct Sums {
+  double n, s1, s2;
 };
-PG_DEV void chan_merge(Moments& a, double nb, double mb, double m2b) {
-  if (nb <= 0.0) return;
-  const double nt = a.n + nb, delta = mb - a.mu;
-  a.mu += delta * nb / nt;
-  a.m2 += m2b + delta * delta * a.n * nb / nt;
-  a.n = nt;
-}
-
-__global__ void bn_stats_finalize_kernel(ChannelMap cm, const float* stat, float* mean, float* istd, float* running,
-                                         long long run_ls, float eps, float mom, int update) {
-  const int l = blockIdx.y, c = blockIdx.x * 32 + threadIdx.x, j = threadIdx.y;
-  __shared__ Moments sm[8][32];
-  Moments a{0.0, 0.0, 0.0};
+constexpr int FIN_MAX_LANES = 32;
+__global__ void __launch_bounds__(32 * FIN_MAX_LANES) bn_stats_finalize_kernel(ChannelMap cm, const float* stat,
+                                                                              float* mean, float* istd, float* running,
+                                                                              long long run_ls, float eps, float mom,
+                                                                              int update) {
+  const int l = blockIdx.y, c = blockIdx.x * 32 + threadIdx.x, j = threadIdx.y, nl = blockDim.y;
+  __shared__ Sums sm[FIN_MAX_LANES][32];
+  Sums a{0.0, 0.0, 0.0};
   const int W = cm.Cp * cm.npack;  // statistic row width
+  const float* base = stat + (long long)l * cm.nslot * 4 * W + (c < cm.Cp ? c : 0);
+  const double K = base[3 * W] > 0.f ? (double)base[0] : 0.0;
   if (c < cm.Cp) {
-    for (int s = j; s < cm.nslot; s += 8)
-      for (int q = 0; q < cm.npack; ++q) {
-        const float* e = stat + ((long long)l * cm.nslot + s) * 4 * W + q * cm.Cp + c;
-        const double nb = e[3 * W];
-        if (nb <= 0.0) continue;
-        const double s1 = e[W], s2 = e[2 * W];
-        chan_merge(a, nb, (double)e[0] + s1 / nb, fmax(s2 - s1 * s1 / nb, 0.0));
+    const int items = cm.nslot * cm.npack;
+    for (int k0 = j; k0 < items; k0 += 4 * nl) {
+      float e0[4], e1[4], e2[4], e3[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // four entries in flight before any is added
+        const int k = k0 + u * nl;
+        e0[u] = e1[u] = e2[u] = e3[u] = 0.f;
+        if (k < items) {
+          const float* e = base + (long long)(k / cm.npack) * 4 * W + (k % cm.npack) * cm.Cp;
+          e0[u] = e[0];
+          e1[u] = e[W];
+          e2[u] = e[2 * W];
+          e3[u] = e[3 * W];
+        }
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double nb = e3[u];
+        if (nb <= 0.0) continue;
+        const double d = (double)e0[u] - K, s1 = e1[u];
+        a.n += nb;
+        a.s1 += s1 + nb * d;
+        a.s2 += (double)e2[u] + 2.0 * d * s1 + nb * d * d;
+      }
+    }
   }
   sm[j][threadIdx.x] = a;
-  __syncthreads();
+  for (int h = nl / 2; h > 0; h >>= 1) {
+    __syncthreads();
+    if (j < h) {
+      const Sums b = sm[j + h][threadIdx.x];
+      a.n += b.n;
+      a.s1 += b.s1;
+      a.s2 += b.s2;
+      sm[j][threadIdx.x] = a;
+    }
+  }
   if (j != 0 || c >= cm.Cp) return;
-  for (int k = 1; k < 8; ++k) chan_merge(a, sm[k][threadIdx.x].n, sm[k][threadIdx.x].mu, sm[k][threadIdx.x].m2);
   const int i = l * cm.Cp + c;
-  const double var = a.n > 0.0 ? a.m2 / a.n : 0.0;
-  mean[i] = (float)a.mu;
+  const double mu = a.n > 0.0 ? K + a.s1 / a.n : 0.0;
+  const double var = a.n > 0.0 ? fmax(a.s2 - a.s1 * (a.s1 / a.n), 0.0) / a.n : 0.0;
+  mean[i] = (float)mu;
   istd[i] = 1.f / sqrtf((float)var + eps);
   if (update && c < cm.C) {
     float* rm = running + (long long)l * run_ls;
     float* rv = rm + cm.C;
     const float m = (float)cm.R;
     const float unbias = m > 1.f ? m / (m - 1.f) : 1.f;
-    rm[c] = (1.f - mom) * rm[c] + mom * (float)a.mu;
+    rm[c] = (1.f - mom) * rm[c] + mom * (float)mu;
     rv[c] = (1.f - mom) * rv[c] + mom * (float)var * unbias;
   }
 }
@@ -245,7 +280,7 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(ChannelMap cm, const floa
       float o4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        o4[u] = c0 + u < cm.C ? act_fwd(act, a[u] * (r[u] - m[u]) + bb[u], slope) : 0.f;
+        o4[u] = c0 + u < cm.C ? act_fwd(act, bn_pre(a[u], r[u], m[u], bb[u]), slope) : 0.f;
       return make_float4(o4[0], o4[1], o4[2], o4[3]);
     };
     long long q = q0;
@@ -270,7 +305,7 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(ChannelMap cm, const floa
       int c = c0 + u;
       if (c < cm.C) {
         long long mc = (long long)l * cm.Cp + c;
-        r[u] = act_fwd(act, gamma[c] * istd[mc] * (r[u] - mean[mc]) + beta[c], slope);
+        r[u] = act_fwd(act, bn_pre(gamma[c] * istd[mc], r[u], mean[mc], beta[c]), slope);
       } else {
         r[u] = 0.f;
       }
@@ -324,27 +359,89 @@ __global__ void bn_bwd_finalize_kernel(ChannelMap cm, const float* partial, cons
   }
 }
 
-__global__ void bn_bwd_apply_kernel(ChannelMap cm, const float* __restrict__ gy, const float* __restrict__ y,
-                                    const float* __restrict__ x, const float* __restrict__ mean,
-                                    const float* __restrict__ coef, int act, float slope, float* __restrict__ gz) {
-  const long long per = (long long)cm.R * cm.Cp / 4;
-  const int l = blockIdx.y;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < per; q += (long long)gridDim.x * blockDim.x) {
-    const long long o = (long long)l * cm.ls + q * 4;
-    const int c0 = (int)((q * 4) % cm.Cp);
-    float4 g4 = *reinterpret_cast<const float4*>(gy + o);
-    float4 y4 = act == ACT_NONE ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(y + o);
-    float4 x4 = *reinterpret_cast<const float4*>(x + o);
-    float g[4] = {g4.x, g4.y, g4.z, g4.w}, yy[4] = {y4.x, y4.y, y4.z, y4.w}, xx[4] = {x4.x, x4.y, x4.z, x4.w};
-    float r[4];
+// Per-channel coefficients of one float4 channel group for bn_bwd_apply.
+struct BwdCoef4 {
+  float cf0[4], cf1[4], cf2[4], m[4], ra[4], rm[4], rb[4];
+};
+PG_DEV void load_bwd_coef(BwdCoef4& k, const ChannelMap& cm, int l, int c0, const float* mean, const float* coef,
+                          const BnCoef& bc, bool rec) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      long long mc = (long long)l * cm.Cp + c0 + u;
-      const float* cf = coef + mc * 3;
-      float g1 = act_bwd(act, g[u], yy[u], slope);
-      r[u] = g1 * cf[0] + cf[1] * (xx[u] - mean[mc]) + cf[2];
+  for (int u = 0; u < 4; ++u) {
+    const int c = c0 + u;
+    const long long mc = (long long)l * cm.Cp + c;
+    k.cf0[u] = coef[mc * 3];
+    k.cf1[u] = coef[mc * 3 + 1];
+    k.cf2[u] = coef[mc * 3 + 2];
+    k.m[u] = mean[mc];
+    const bool ok = rec && c < cm.C;
+    // as bn_apply holds them (a = gamma istd, zero coefficients on padding channels)
+    k.ra[u] = ok ? bc.gb[(long long)l * bc.gb_ls + c] * bc.istd[mc] : 0.f;
+    k.rm[u] = ok ? k.m[u] : 0.f;
+    k.rb[u] = ok ? bc.gb[(long long)l * bc.gb_ls + cm.C + c] : 0.f;
+  }
+}
+PG_DEV float4 bwd_apply4(const BwdCoef4& k, int act, float slope, bool rec, float4 g4, float4 y4, float4 x4) {
+  const float g[4] = {g4.x, g4.y, g4.z, g4.w}, xx[4] = {x4.x, x4.y, x4.z, x4.w};
+  float yy[4] = {y4.x, y4.y, y4.z, y4.w}, r[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (rec) yy[u] = act_fwd(act, bn_pre(k.ra[u], xx[u], k.rm[u], k.rb[u]), slope);
+    const float g1 = act_bwd(act, g[u], yy[u], slope);
+    r[u] = g1 * k.cf0[u] + k.cf1[u] * (xx[u] - k.m[u]) + k.cf2[u];
+  }
+  return make_float4(r[0], r[1], r[2], r[3]);
+}
+
+// gz = act_bwd(gy, y) gamma istd + 2 dvar (x - mean) / m + dmean / m.  With
+// bc.istd (ReLU / LeakyReLU) y is recomputed from x instead of read.  When the
+// grid stride is a multiple of the row width each thread keeps one channel
+// group and its coefficients in registers, four float4 loads of each map in flight.
+__global__ void __launch_bounds__(256) bn_bwd_apply_kernel(ChannelMap cm, const float* __restrict__ gy,
+                                                           const float* __restrict__ y, const float* __restrict__ x,
+                                                           const float* __restrict__ mean,
+                                                           const float* __restrict__ coef, int act, float slope,
+                                                           float* __restrict__ gz, BnCoef bc) {
+  const int c4n = cm.Cp / 4;
+  const long long per = (long long)cm.R * c4n;
+  const int l = blockIdx.y;
+  const bool rec = bc.istd != nullptr && sign_act(act);
+  const bool ld_y = act != ACT_NONE && !rec;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long q0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const float* gl = gy + (long long)l * cm.ls;
+  const float* yl = y + (long long)l * cm.ls;
+  const float* xl = x + (long long)l * cm.ls;
+  float* ol = gz + (long long)l * cm.ls;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  BwdCoef4 k;
+  if (stride % c4n == 0) {
+    load_bwd_coef(k, cm, l, (int)(q0 % c4n) * 4, mean, coef, bc, rec);
+    long long q = q0;
+    for (; q + 3 * stride < per; q += 4 * stride) {
+      float4 g4[4], y4[4], x4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const long long o = (q + j * stride) * 4;
+        g4[j] = ld4(gl + o);
+        x4[j] = ld4(xl + o);
+        y4[j] = ld_y ? ld4(yl + o) : z4;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<float4*>(ol + (q + j * stride) * 4) = bwd_apply4(k, act, slope, rec, g4[j], y4[j], x4[j]);
     }
-    *reinterpret_cast<float4*>(gz + o) = make_float4(r[0], r[1], r[2], r[3]);
+    for (; q < per; q += stride) {
+      const long long o = q * 4;
+      *reinterpret_cast<float4*>(ol + o) =
+          bwd_apply4(k, act, slope, rec, ld4(gl + o), ld_y ? ld4(yl + o) : z4, ld4(xl + o));
+    }
+    return;
+  }
+  for (long long q = q0; q < per; q += stride) {
+    const long long o = q * 4;
+    load_bwd_coef(k, cm, l, (int)(q % c4n) * 4, mean, coef, bc, rec);
+    *reinterpret_cast<float4*>(ol + o) =
+        bwd_apply4(k, act, slope, rec, ld4(gl + o), ld_y ? ld4(yl + o) : z4, ld4(xl + o));
   }
 }
 
@@ -587,10 +684,17 @@ cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* m
   return launched();
 }
 
+// lanes per channel: about 8 entries per lane, 4..32 (few entries: small blocks)
+static int fin_lanes(const ChannelMap& cm) {
+  int nl = 4;
+  while (nl < FIN_MAX_LANES && nl * 8 < cm.nslot * cm.npack) nl <<= 1;
+  return nl;
+}
+
 cudaError_t launch_bn_stats_finalize(const ChannelMap& cm, const float* stat, float* mean, float* istd, float* running,
                                      long long run_ls, float eps, float momentum, int update_running, cudaStream_t st) {
   if (cm.nslot <= 0) return cudaErrorInvalidValue;
-  bn_stats_finalize_kernel<<<dim3((cm.Cp + 31) / 32, cm.L), dim3(32, 8), 0, st>>>(cm, stat, mean, istd, running,
+  bn_stats_finalize_kernel<<<dim3((cm.Cp + 31) / 32, cm.L), dim3(32, fin_lanes(cm)), 0, st>>>(cm, stat, mean, istd, running,
                                                                                   run_ls, eps, momentum,
                                                                                   update_running);
   return launched();
@@ -614,9 +718,11 @@ cudaError_t launch_bn_bwd_finalize(const ChannelMap& cm, const float* partial, c
 
 cudaError_t launch_bn_bwd_apply(const ChannelMap& cm, const float* gy, const float* y, const float* x,
                                 const float* mean, const float* coef, int act, float slope, float* gz,
-                                cudaStream_t st) {
-  dim3 grid(grid_for((long long)cm.R * cm.Cp / 4, 256, 4096), cm.L);
-  bn_bwd_apply_kernel<<<grid, 256, 0, st>>>(cm, gy, y, x, mean, coef, act, slope, gz);
+                                cudaStream_t st, BnCoef bc) {
+  const long long per = (long long)cm.R * cm.Cp / 4;
+  const unsigned cap = std::max(1u, 148u * 8u / (unsigned)std::max(1, cm.L));
+  dim3 grid(grid_for(per, 256 * 16, cap), cm.L);
+  bn_bwd_apply_kernel<<<grid, 256, 0, st>>>(cm, gy, y, x, mean, coef, act, slope, gz, bc);
   return launched();
 }
 

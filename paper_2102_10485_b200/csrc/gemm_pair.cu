@@ -293,6 +293,17 @@ __host__ __device__ constexpr int lo_stages(int bn, bool split) { return split ?
 __host__ __device__ constexpr int hi_stages(int bn, bool split) {
   return total_stages(bn) - lo_stages(bn, split) > 8 ? 8 : total_stages(bn) - lo_stages(bn, split);
 }
+#ifndef PG_PF_NARROW
+#define PG_PF_NARROW 0
+#endif
+#ifndef PG_PF_WIDE
+#define PG_PF_WIDE 0
+#endif
+// L2 prefetch distance in k-blocks (0 = off).  Measured slower at every
+// distance tried (4 / 8 / 16 narrow, 8 wide; up to 1.8x on the conv2 weight
+// gradient): the narrow tiles are shared-memory-bandwidth bound, not latency
+// bound, and the extra TMA requests only compete.
+__host__ __device__ constexpr int pf_dist(int bn, bool split) { return bn >= 256 ? PG_PF_WIDE : PG_PF_NARROW; }
 __host__ __device__ constexpr int smem_total(int bn, bool split) {
   return (hi_stages(bn, split) + lo_stages(bn, split)) * stage_bytes(bn) + 1024 + 1024;
 }
@@ -310,7 +321,7 @@ PG_DEV void pair_tile_decode(const PairPlan& P, int t, int& label, int& phase, i
 __host__ __device__ constexpr int seg_bufs(int bn) { return 512 / bn > 4 ? 4 : 512 / bn; }
 
 // TMA boxes of k-block kb for this CTA: its 128 A rows and its B half
-template <int KIND, int BH>
+template <int KIND, int BH, bool PF = false>
 PG_DEV void pair_issue(const CUtensorMap& tmA, const CUtensorMap& tmB, const PairPlan& P, uint32_t a_dst,
                        uint32_t b_dst, uint64_t* bar, int kb, int label, int mtp, uint32_t rank, int n0, int b0,
                        int i0, int j0, const DgPhase& d) {
@@ -323,24 +334,24 @@ PG_DEV void pair_issue(const CUtensorMap& tmA, const CUtensorMap& tmB, const Pai
     for (int t = 0; t < BKT / 4; ++t) {
       const int tap = kb * (BKT / 4) + t;
       const int ki = tap / g.k, kj = tap % g.k;
-      tma_load_5d(a_dst + t * (BM * 16), &tmA, bar, 0, j0 * g.s - g.p + kj, i0 * g.s - g.p + ki, b0, label);
+      tbox<PF>(a_dst + t * (BM * 16), &tmA, bar, 0, j0 * g.s - g.p + kj, i0 * g.s - g.p + ki, b0, label);
     }
-    tma_load_3d(b_dst, &tmB, bar, kb * BKT, n0, label);
+    tbox<PF>(b_dst, &tmB, bar, kb * BKT, n0, label);
   } else if (KIND == GEMM_FPROP) {
     const int tap = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
     const int ki = tap / g.k, kj = tap % g.k;
-    tma_load_5d(a_dst, &tmA, bar, c0, j0 * g.s - g.p + kj, i0 * g.s - g.p + ki, b0, label);
-    tma_load_3d(b_dst, &tmB, bar, kb * BKT, n0, label);
+    tbox<PF>(a_dst, &tmA, bar, c0, j0 * g.s - g.p + kj, i0 * g.s - g.p + ki, b0, label);
+    tbox<PF>(b_dst, &tmB, bar, kb * BKT, n0, label);
   } else if (KIND == KIND_DGP) {
     // k-block = (neighbour (di, dj) of the 2x2 small-map block, 32 input channels)
     const int nbr = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
     const int di = nbr >> 1, dj = nbr & 1;
-    tma_load_5d(a_dst, &tmA, bar, c0, j0 - dj, i0 - di, b0, label);
+    tbox<PF>(a_dst, &tmA, bar, c0, j0 - dj, i0 - di, b0, label);
 #pragma unroll
     for (int q = 0; q < BH / 32; ++q) {
       const int n = n0 + 32 * q, ph = n / g.CG;
       const int ki = (ph >> 1) + 2 * di, kj = (ph & 1) + 2 * dj;
-      tma_load_4d(b_dst + q * (BKT * 128), &tmB, bar, n % g.CG, ki * g.k + kj, c0, label);
+      tbox<PF>(b_dst + q * (BKT * 128), &tmB, bar, n % g.CG, ki * g.k + kj, c0, label);
     }
   } else if (KIND == GEMM_DGRAD) {
     const int tp = kb / P.kcb, c0 = (kb % P.kcb) * BKT;
@@ -348,10 +359,10 @@ PG_DEV void pair_issue(const CUtensorMap& tmA, const CUtensorMap& tmB, const Pai
     const int ki = d.ry + ty * g.s, kj = d.rx + tx * g.s;
     const int offy = (d.y0 + g.p - d.ry) / g.s - ty;
     const int offx = (d.x0 + g.p - d.rx) / g.s - tx;
-    tma_load_5d(a_dst, &tmA, bar, c0, j0 + offx, i0 + offy, b0, label);
+    tbox<PF>(a_dst, &tmA, bar, c0, j0 + offx, i0 + offy, b0, label);
 #pragma unroll
     for (int q = 0; q < BH / 32; ++q)
-      tma_load_4d(b_dst + q * (BKT * 128), &tmB, bar, n0 + 32 * q, ki * g.k + kj, c0, label);
+      tbox<PF>(b_dst + q * (BKT * 128), &tmB, bar, n0 + 32 * q, ki * g.k + kj, c0, label);
   } else {
     int kb0, ki0, kj0;
     box_origin(P.box, kb, kb0, ki0, kj0);
@@ -361,12 +372,12 @@ PG_DEV void pair_issue(const CUtensorMap& tmA, const CUtensorMap& tmB, const Pai
       const int m = m0 + 32 * q;
       const int tap = m / g.CG, cg0 = m % g.CG;
       const int ki = tap / g.k, kj = tap % g.k;
-      tma_load_5d(a_dst + q * (BKT * 128), &tmA, bar, cg0, kj0 * g.s - g.p + kj,
+      tbox<PF>(a_dst + q * (BKT * 128), &tmA, bar, cg0, kj0 * g.s - g.p + kj,
           ki0 * g.s - g.p + ki, kb0, label);
     }
 #pragma unroll
     for (int q = 0; q < BH / 32; ++q)
-      tma_load_5d(b_dst + q * (BKT * 128), &tmB, bar, n0 + 32 * q, kj0, ki0, kb0, label);
+      tbox<PF>(b_dst + q * (BKT * 128), &tmB, bar, n0 + 32 * q, kj0, ki0, kb0, label);
   }
 }
 
@@ -525,22 +536,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
+      // opt-in: the boxes of k-block kb + PFD are prefetched into L2 when kb is
+      // loaded (pf_dist; off by default, see there)
+      struct TileAt {
+        int label, mtp, n0, b0, i0, j0;
+        DgPhase d;
+      };
+      auto tile_at = [&](int t) {
+        TileAt x{};
+        int phase, nt;
+        pair_tile_decode(P, t, x.label, phase, x.mtp, nt);
+        x.n0 = nt * BN + (int)rank * BH;  // this CTA's B half
+        if (KIND != GEMM_WGRAD) box_origin(P.box, 2 * x.mtp + (int)rank, x.b0, x.i0, x.j0);
+        if (KIND == GEMM_DGRAD) x.d = dg_phase(g, phase);
+        return x;
+      };
+      constexpr int PFD = pf_dist(BN, SPLIT);
       uint32_t it = 0;
       for (int t = cl; t < ntiles; t += ncl) {
-        int label, phase, mtp, nt;
-        pair_tile_decode(P, t, label, phase, mtp, nt);
-        const int n0 = nt * BN + (int)rank * BH;  // this CTA's B half
-        int b0 = 0, i0 = 0, j0 = 0;
-        if (KIND != GEMM_WGRAD) box_origin(P.box, 2 * mtp + (int)rank, b0, i0, j0);
-        DgPhase d{};
-        if (KIND == GEMM_DGRAD) d = dg_phase(g, phase);
+        const TileAt c = tile_at(t);
+        TileAt nx{};
+        const bool has_next = PFD > 0 && t + ncl < ntiles;
+        if (has_next) nx = tile_at(t + ncl);
         for (int kb = 0; kb < P.nk; ++kb, ++it) {
           const int s = it % SH;
           mbar_wait(empty_h + s, ((it / SH) & 1) ^ 1);
           mbar_expect_tx(full_h + s, P.stage_tx);
           const uint32_t a_dst = smem_u32(smem + s * SB);
           const uint32_t b_dst = a_dst + AB;
-          pair_issue<KIND, BH>(tmA, tmB, P, a_dst, b_dst, full_h + s, kb, label, mtp, rank, n0, b0, i0, j0, d);
+          pair_issue<KIND, BH>(tmA, tmB, P, a_dst, b_dst, full_h + s, kb, c.label, c.mtp, rank, c.n0, c.b0, c.i0,
+                               c.j0, c.d);
+          if (PFD > 0) {
+            const int kp = kb + PFD;
+            if (kp < P.nk)
+              pair_issue<KIND, BH, true>(tmA, tmB, P, 0, 0, nullptr, kp, c.label, c.mtp, rank, c.n0, c.b0, c.i0, c.j0,
+                                         c.d);
+            else if (has_next && kp - P.nk < P.nk)
+              pair_issue<KIND, BH, true>(tmA, tmB, P, 0, 0, nullptr, kp - P.nk, nx.label, nx.mtp, rank, nx.n0, nx.b0,
+                                         nx.i0, nx.j0, nx.d);
+          }
         }
       }
     }

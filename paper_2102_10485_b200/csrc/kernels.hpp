@@ -65,6 +65,15 @@ int reduce_chunks(const ChannelMap& cm);
 size_t reduce_partial_floats(const ChannelMap& cm);
 // partial: [L][chunks][3][Cp]
 // RED_ACT_G with g_out: also writes g1 = act_bwd(gy, y) (activation backward + bias sums in one pass)
+// BN coefficients of a block (istd [L][Cp], gamma/beta at gb + l gb_ls): given
+// to bn_bwd_apply, it recomputes a ReLU / LeakyReLU output from the pre-BN map
+// instead of reading the stored y (bit-identical, see bn_pre).  Measured: 21%
+// off bn_bwd_apply; the same recompute in channel_reduce made it 9% slower.
+struct BnCoef {
+  const float* istd = nullptr;
+  const float* gb = nullptr;
+  long long gb_ls = 0;
+};
 cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x, const float* gy, const float* y,
                                   const float* mean, int act, float slope, float* partial, cudaStream_t st,
                                   float* g_out = nullptr);
@@ -95,7 +104,7 @@ cudaError_t launch_bn_bwd_finalize(const ChannelMap& cm, const float* partial, c
 // gz = act_bwd(gy, y) * gamma istd + dvar 2 (x - mean)/m + dmean/m
 cudaError_t launch_bn_bwd_apply(const ChannelMap& cm, const float* gy, const float* y, const float* x,
                                 const float* mean, const float* coef, int act, float slope, float* gz,
-                                cudaStream_t st);
+                                cudaStream_t st, BnCoef bc = {});
 // g = act_bwd(gy, y) elementwise (in place allowed)
 cudaError_t launch_act_bwd(const ChannelMap& cm, const float* gy, const float* y, int act, float slope, float* g,
                            cudaStream_t st);

@@ -570,6 +570,12 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
     float* dbias = param_grads ? grads.p + b.off_b : nullptr;
     bool bias_done = false;
     if (b.has_bn) {
+      // bn_bwd_apply takes the activation mask from (pre-BN map, BN coefficients), not the stored y
+      static const bool yfree = [] {
+        const char* e = std::getenv("PG_YFREE");  // 0: read the stored y (A/B timing)
+        return !(e && e[0] == '0');
+      }();
+      const BnCoef bnc = yfree ? BnCoef{t.istd[i].p, params.p + b.off_bn, P_} : BnCoef{};
       ChannelMap cs = cm;
       if (fused) {
         // sums from the producing GEMM's epilogue, pre-reduced over its slots
@@ -590,7 +596,7 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
                  "bn bwd finalize");
       bias_done = closed_form_bias;
       check_cuda(launch_bn_bwd_apply(cm, gy, t.act[i + 1], t.pre[i].p, t.mean[i].p, coef_.p, fused ? ACT_NONE : b.act,
-                                     b.slope, gz_.p, st),
+                                     b.slope, gz_.p, st, bnc),
                  "bn bwd apply");
       gz = gz_.p;
     } else if (b.act != ACT_NONE && !fused) {

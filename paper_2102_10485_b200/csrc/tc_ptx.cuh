@@ -122,6 +122,36 @@ PG_DEV void tma_load_5d(uint32_t dst, const void* tmap, uint64_t* bar, int c0, i
       : "memory");
 }
 
+// L2 prefetch of the box a tma_load_Nd with the same coordinates would fetch
+PG_DEV void tma_pf_3d(const void* tmap, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+PG_DEV void tma_pf_4d(const void* tmap, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+PG_DEV void tma_pf_5d(const void* tmap, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+// load (PF = false) or L2-prefetch (PF = true) of one box
+template <bool PF>
+PG_DEV void tbox(uint32_t dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2) {
+  if (PF) tma_pf_3d(tmap, c0, c1, c2); else tma_load_3d(dst, tmap, bar, c0, c1, c2);
+}
+template <bool PF>
+PG_DEV void tbox(uint32_t dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2, int c3) {
+  if (PF) tma_pf_4d(tmap, c0, c1, c2, c3); else tma_load_4d(dst, tmap, bar, c0, c1, c2, c3);
+}
+template <bool PF>
+PG_DEV void tbox(uint32_t dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2, int c3, int c4) {
+  if (PF) tma_pf_5d(tmap, c0, c1, c2, c3, c4); else tma_load_5d(dst, tmap, bar, c0, c1, c2, c3, c4);
+}
+
 // one lane of the (fully active) warp: the lowest; the same lane every call
 PG_DEV bool elect_one() {
   uint32_t pred = 0;
