@@ -120,7 +120,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
   cudaError_t r;
   if (math != MATH_FP32_SIMT && lowered_enabled(a) && gemm_lowered_supported(a)) r = launch_gemm_lowered(a, math, st);
   else if (math != MATH_FP32_SIMT && image_side_direct(a)) r = launch_gemm_pair(a, math, st);  // 4-channel FPROP
-  else if (gemm_thin_supported(a)) r = launch_gemm_thin(a, st);  // image-side / dense-head shapes (fp32 FMA)
+  else if (gemm_thin_supported(a)) r = launch_gemm_thin(a, st, math);  // image-side / dense-head shapes
   else if (math != MATH_FP32_SIMT && gemm_pair_supported(a)) r = launch_gemm_pair(a, math, st);  // big conv GEMMs
   else if (math != MATH_FP32_SIMT && gemm_tma_supported(a)) r = launch_gemm_tma(a, math, st);  // conv GEMMs
   else if (math != MATH_FP32_SIMT && gemm_tc_supported(a)) r = launch_gemm_tc(a, math, st);

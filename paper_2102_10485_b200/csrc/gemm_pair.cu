@@ -442,12 +442,31 @@ PG_DEV void pair_drain_role(const PairPlan& P, uint32_t tmem, uint64_t* seg_full
         const int m = mtp * (2 * BM) + (int)rank * BM + row;
         if (m < P.mrows) {
           float* base = P.out + (long long)label * P.out_ls + m;
+          if (P.accumulate) {
+            // read-modify-write in batches of 32 columns, all loads issued
+            // before any store: with load / store interleaved per column (the
+            // stores may alias the next load) every column paid a full memory
+            // latency -- 3.6x on the second pass of the discriminator weight
+            // gradient (real + fake)
 #pragma unroll
-          for (int c = 0; c < BH; ++c) {
-            const int n = nb + c;
-            if (n < P.N) {
-              float* dst = base + (long long)n * P.mrows;
-              *dst = P.accumulate ? *dst + acc[c] : acc[c];
+            for (int c0 = 0; c0 < BH; c0 += 32) {
+              float old[32];
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const int n = nb + c0 + c;
+                old[c] = n < P.N ? base[(long long)n * P.mrows] : 0.f;
+              }
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const int n = nb + c0 + c;
+                if (n < P.N) base[(long long)n * P.mrows] = old[c] + acc[c0 + c];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < BH; ++c) {
+              const int n = nb + c;
+              if (n < P.N) base[(long long)n * P.mrows] = acc[c];
             }
           }
         }

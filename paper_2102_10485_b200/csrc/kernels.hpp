@@ -40,7 +40,8 @@ int gemm_lowered_stat_slots(const GemmArgs& a);
 // GEMM columns per output channel (4 for phase-packed DGRAD: stat rows are
 // npack * N_out wide, channel c at columns c + q N_out)
 int gemm_stat_slots(const GemmArgs& a, int math, int* npack = nullptr);
-cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st);  // thin.cu
+// thin.cu; math selects the 4-channel weight gradient's form (TF32 modes: mma.sync tensor cores)
+cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math = MATH_FP32_SIMT);
 bool gemm_thin_supported(const GemmArgs& a);
 float* gemm_scratch(size_t floats, cudaStream_t st);  // grow-only workspace for split-K reductions
 // picks the engine for a math mode and problem shape

@@ -279,6 +279,101 @@ __global__ void __launch_bounds__(256) thin_in_wgrad_partial_kernel(GemmArgs a, 
         make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
 }
 
+// Tensor-core form of the same partial GEMM (TF32X3 / TF32 math): the legacy
+// warp-level mma.sync m16n8k8 TF32 path -- M = N = 64 is far too narrow for a
+// CTA-pair tcgen05 tile, and the SIMT loop above runs at the FP32 FMA roof.
+// Block = (chunk, label), 8 warps; warp w owns rows 16 (w / 2) .. + 16 and
+// columns 32 (w % 2) .. + 32 of the 64 x 64 partial (four n8 tiles).  The 3xTF32
+// split is the tcgen05 path's: hi = the fp32 bits truncated by the tensor core,
+// lo = x - trunc(x); products small terms first.
+constexpr int TWM_LD = 72;  // smem row pitch (floats): fragment loads conflict-free
+PG_DEV void mma_tf32_16x8x8(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+PG_DEV uint32_t tf32_lo(float x) { return __float_as_uint(x - __uint_as_float(__float_as_uint(x) & 0xffffe000u)); }
+
+template <bool X3>
+__global__ void __launch_bounds__(256) thin_in_wgrad_mma_kernel(GemmArgs a, float* part, int nchunk) {
+  const ConvGeo& g = a.g;
+  const int l = blockIdx.y, chunk = blockIdx.x;
+  const int kk = g.k * g.k;
+  const float* sg = a.small + l * a.small_ls;
+  const float* big = a.big + l * a.big_ls;
+  __shared__ __align__(16) float gs[TW_KC][TWM_LD];
+  __shared__ __align__(16) float xs[TW_KC][TWM_LD];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int lq = tid / 8, lp = tid % 8;  // loader: pixel lq of the stage, float4 slots lp and lp + 8
+  const int fg = lane >> 2, ft = lane & 3;  // fragment row group / thread in group
+  const int m0 = (warp >> 1) * 16, n0 = (warp & 1) * 32;
+  float acc[4][4] = {};
+  const long long K = (long long)g.B * g.SH * g.SW;
+  const long long k_begin = (long long)chunk * TW_SPLIT;
+  const long long k_end = k_begin + TW_SPLIT < K ? k_begin + TW_SPLIT : K;
+  float4 ra[2], rb[2];
+  auto fetch = [&](long long k0) {
+    const long long sp = k0 + lq;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    ra[0] = ra[1] = rb[0] = rb[1] = z;
+    if (sp >= k_end) return;
+    const int j = (int)(sp % g.SW);
+    const long long t = sp / g.SW;
+    const int i = (int)(t % g.SH), b = (int)(t / g.SH);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int slot = lp + 8 * h;
+      if (slot * 4 < g.CS) ra[h] = __ldg(reinterpret_cast<const float4*>(sg + sp * g.CS) + slot);
+      if (slot < kk) {
+        const int y = i * g.s - g.p + slot / g.k, x = j * g.s - g.p + slot % g.k;
+        if (y >= 0 && y < g.GH && x >= 0 && x < g.GW)
+          rb[h] = __ldg(reinterpret_cast<const float4*>(big + (((long long)b * g.GH + y) * g.GW + x) * 4));
+      }
+    }
+  };
+  fetch(k_begin);
+  for (long long k0 = k_begin; k0 < k_end; k0 += TW_KC) {
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      *reinterpret_cast<float4*>(&gs[lq][4 * (lp + 8 * h)]) = ra[h];
+      *reinterpret_cast<float4*>(&xs[lq][4 * (lp + 8 * h)]) = rb[h];
+    }
+    __syncthreads();
+    if (k0 + TW_KC < k_end) fetch(k0 + TW_KC);
+#pragma unroll
+    for (int q = 0; q < TW_KC; q += 8) {
+      // A[m][k] = gs[k][m], B[k][n] = xs[k][n]
+      const float af[4] = {gs[q + ft][m0 + fg], gs[q + ft][m0 + fg + 8], gs[q + ft + 4][m0 + fg],
+                           gs[q + ft + 4][m0 + fg + 8]};
+      uint32_t ah[4], al[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ah[u] = __float_as_uint(af[u]);
+        al[u] = tf32_lo(af[u]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const float b0 = xs[q + ft][n0 + nt * 8 + fg], b1 = xs[q + ft + 4][n0 + nt * 8 + fg];
+        if (X3) {
+          mma_tf32_16x8x8(acc[nt], al, __float_as_uint(b0), __float_as_uint(b1));
+          mma_tf32_16x8x8(acc[nt], ah, tf32_lo(b0), tf32_lo(b1));
+        }
+        mma_tf32_16x8x8(acc[nt], ah, __float_as_uint(b0), __float_as_uint(b1));
+      }
+    }
+  }
+  float* dst = part + ((long long)l * nchunk + chunk) * 64 * 64;
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const int n = n0 + nt * 8 + 2 * ft;
+    *reinterpret_cast<float2*>(dst + (m0 + fg) * 64 + n) = make_float2(acc[nt][0], acc[nt][1]);
+    *reinterpret_cast<float2*>(dst + (m0 + fg + 8) * 64 + n) = make_float2(acc[nt][2], acc[nt][3]);
+  }
+}
+
 __global__ void thin_in_wgrad_reduce_kernel(GemmArgs a, const float* part, int nchunk) {
   const ConvGeo& g = a.g;
   const int l = blockIdx.y;
@@ -443,7 +538,7 @@ Thin classify(const GemmArgs& a) {
 
 bool gemm_thin_supported(const GemmArgs& a) { return classify(a) != T_NONE; }
 
-cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st) {
+cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math) {
   const ConvGeo& g = a.g;
   switch (classify(a)) {
     case T_OUT_DGRAD: {
@@ -481,7 +576,12 @@ cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st) {
       const int nchunk = (int)((K + TW_SPLIT - 1) / TW_SPLIT);
       float* part = gemm_scratch((size_t)a.L * nchunk * 64 * 64, st);
       if (!part) return cudaErrorMemoryAllocation;
-      thin_in_wgrad_partial_kernel<<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
+      if (math == MATH_TF32X3)
+        thin_in_wgrad_mma_kernel<true><<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
+      else if (math == MATH_TF32)
+        thin_in_wgrad_mma_kernel<false><<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
+      else
+        thin_in_wgrad_partial_kernel<<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
       cudaError_t e = launched();
       if (e != cudaSuccess) return e;
       const int nout = g.CS * g.k * g.k * 4;
