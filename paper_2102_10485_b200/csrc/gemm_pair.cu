@@ -46,8 +46,14 @@ constexpr int BKT = 32;   // fp32 of K per k-block (one 128-byte row)
 // which take half as long on BN <= 128 tiles (measured: 2 warps paced the
 // narrow tiles in TF32X3 once MMA issue was warp-uniform)
 // (FPROP / DGRAD in TF32X3; the WGRAD tiles measured slower with 4: 1.45 vs 1.35 ms)
+#ifndef PG_NSPLIT_NARROW
+#define PG_NSPLIT_NARROW 4
+#endif
+#ifndef PG_NSPLIT_WG
+#define PG_NSPLIT_WG 2
+#endif
 __host__ __device__ constexpr int nsplit(int kind, int bn, int mode) {
-  return bn <= 128 && kind != GEMM_WGRAD && mode == MATH_TF32X3 ? 4 : 2;
+  return mode != MATH_TF32X3 || bn > 128 ? 2 : kind == GEMM_WGRAD ? PG_NSPLIT_WG : PG_NSPLIT_NARROW;
 }
 __host__ __device__ constexpr int pair_nt(int kind, int bn, int mode) { return (nsplit(kind, bn, mode) + 2 + 8) * 32; }
 constexpr int NDRAIN = 8;
