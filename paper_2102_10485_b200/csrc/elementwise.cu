@@ -36,18 +36,23 @@ PG_DEV float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>
 PG_DEV float bn_pre(float a, float x, float m, float b) { return __fmaf_rn(a, x - m, b); }
 // the activation backward of a BN block can be taken from (x, BN coefficients)
 // instead of a stored y when the derivative depends on y only through its sign
-PG_DEV bool sign_act(int act) { return act == ACT_RELU || act == ACT_LRELU; }
+__host__ __device__ inline bool sign_act(int act) { return act == ACT_RELU || act == ACT_LRELU; }
 
 // Per-channel sums over the rows of [L][R][Cp] maps.  Block = (label, chunk of
 // red_rows(cm) rows, up to 256 float4 channel groups): a thread owns 4 channels
 // (float4 loads along the row) and a row lane; the row lanes are combined in
 // shared memory in a fixed order, and the chunk partials by the finalize
-// kernels in chunk order (deterministic, no atomics).
-__global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, int mode, const float* __restrict__ x,
+// kernels in chunk order (deterministic, no atomics).  Mode and activation are
+// template parameters (straight-line loop bodies: the loads of several rows
+// are issued together).  REC (RED_BN_BWD, ReLU / LeakyReLU): the activation
+// output is recomputed from x and the BN coefficients (bn_pre) instead of read.
+template <int MODE, int ACT, bool REC>
+__global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, const float* __restrict__ x,
                                                                 const float* __restrict__ gy,
                                                                 const float* __restrict__ y,
-                                                                const float* __restrict__ mean, int act, float slope,
-                                                                float* __restrict__ partial, float* __restrict__ g_out) {
+                                                                const float* __restrict__ mean, float slope,
+                                                                float* __restrict__ partial, float* __restrict__ g_out,
+                                                                BnCoef bc) {
   const int l = blockIdx.z, chunk = blockIdx.x, nchunk = gridDim.x;
   const int c4n = cm.Cp / 4;
   const int gpb = c4n < RED_NT ? c4n : RED_NT;  // channel groups per block
@@ -56,27 +61,48 @@ __global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, i
   const int g = blockIdx.y * gpb + gi;
   float4 s0 = f4(0.f), s1 = f4(0.f), s2 = f4(0.f);
   if (g < c4n && lr < lanes) {
-    const float4 mu = (mode == RED_SQDEV || mode == RED_BN_BWD) ? ld4(mean + (long long)l * cm.Cp + 4 * g) : f4(0.f);
+    const float4 mu = (MODE == RED_SQDEV || MODE == RED_BN_BWD) ? ld4(mean + (long long)l * cm.Cp + 4 * g) : f4(0.f);
+    float ra[4] = {0.f, 0.f, 0.f, 0.f}, rm[4] = {0.f, 0.f, 0.f, 0.f}, rb[4] = {0.f, 0.f, 0.f, 0.f};
+    if (REC) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = 4 * g + u;
+        const long long mc = (long long)l * cm.Cp + c;
+        if (c < cm.C) {  // as bn_apply holds them (zero on padding channels)
+          ra[u] = bc.gb[(long long)l * bc.gb_ls + c] * bc.istd[mc];
+          rm[u] = mean[mc];
+          rb[u] = bc.gb[(long long)l * bc.gb_ls + cm.C + c];
+        }
+      }
+    }
     const long long base = (long long)l * cm.ls + 4 * g;
     const int rows = red_rows(cm);
     const int r_end = min(cm.R, (chunk + 1) * rows);
 #pragma unroll 4
     for (int r = chunk * rows + lr; r < r_end; r += lanes) {
       const long long o = base + (long long)r * cm.Cp;
-      if (mode == RED_SUM) {
+      if (MODE == RED_SUM) {
         s0 = add4(s0, ld4(x + o));
-      } else if (mode == RED_SQDEV) {
+      } else if (MODE == RED_SQDEV) {
         const float4 v = ld4(x + o);
         const float dx = v.x - mu.x, dy = v.y - mu.y, dz = v.z - mu.z, dw = v.w - mu.w;
         s0 = add4(s0, make_float4(dx * dx, dy * dy, dz * dz, dw * dw));
       } else {
-        const float4 g4 = ld4(gy + o), y4 = ld4(y + o);
-        const float4 g1 = make_float4(act_bwd(act, g4.x, y4.x, slope), act_bwd(act, g4.y, y4.y, slope),
-                                      act_bwd(act, g4.z, y4.z, slope), act_bwd(act, g4.w, y4.w, slope));
+        const float4 g4 = ld4(gy + o);
+        const float4 v = MODE == RED_BN_BWD ? ld4(x + o) : f4(0.f);
+        float4 y4;
+        if (REC)
+          y4 = make_float4(act_fwd(ACT, bn_pre(ra[0], v.x, rm[0], rb[0]), slope),
+                           act_fwd(ACT, bn_pre(ra[1], v.y, rm[1], rb[1]), slope),
+                           act_fwd(ACT, bn_pre(ra[2], v.z, rm[2], rb[2]), slope),
+                           act_fwd(ACT, bn_pre(ra[3], v.w, rm[3], rb[3]), slope));
+        else
+          y4 = ACT == ACT_NONE ? f4(0.f) : ld4(y + o);
+        const float4 g1 = make_float4(act_bwd(ACT, g4.x, y4.x, slope), act_bwd(ACT, g4.y, y4.y, slope),
+                                      act_bwd(ACT, g4.z, y4.z, slope), act_bwd(ACT, g4.w, y4.w, slope));
         s0 = add4(s0, g1);
-        if (g_out) *reinterpret_cast<float4*>(g_out + o) = g1;  // RED_ACT_G: the activation backward itself
-        if (mode == RED_BN_BWD) {
-          const float4 v = ld4(x + o);
+        if (MODE == RED_ACT_G && g_out) *reinterpret_cast<float4*>(g_out + o) = g1;  // the activation backward itself
+        if (MODE == RED_BN_BWD) {
           const float4 d = make_float4(v.x - mu.x, v.y - mu.y, v.z - mu.z, v.w - mu.w);
           s1 = add4(s1, make_float4(g1.x * d.x, g1.y * d.y, g1.z * d.z, g1.w * d.w));
           s2 = add4(s2, d);
@@ -90,7 +116,7 @@ __global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, i
   sm[2][t] = s2;
   __syncthreads();
   if (lr != 0 || g >= c4n) return;
-  const int nk = mode == RED_BN_BWD ? 3 : 1;
+  const int nk = MODE == RED_BN_BWD ? 3 : 1;
   for (int k = 0; k < 3; ++k) {
     float4 acc = f4(0.f);
     if (k < nk)
@@ -642,12 +668,33 @@ size_t reduce_partial_floats(const ChannelMap& cm) { return (size_t)cm.L * ((cm.
 
 cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x, const float* gy, const float* y,
                                   const float* mean, int act, float slope, float* partial, cudaStream_t st,
-                                  float* g_out) {
+                                  float* g_out, BnCoef bc) {
   if (cm.Cp % 4) return cudaErrorInvalidValue;
   const int c4n = cm.Cp / 4, gpb = c4n < RED_NT ? c4n : RED_NT;
   dim3 grid(reduce_chunks(cm), (c4n + gpb - 1) / gpb, cm.L);
-  channel_reduce_kernel<<<grid, RED_NT, 0, st>>>(cm, mode, x, gy, y, mean, act, slope, partial,
-                                                  mode == RED_ACT_G ? g_out : nullptr);
+  const bool rec = mode == RED_BN_BWD && bc.istd != nullptr && sign_act(act);
+#define PG_RED(M, A, R) channel_reduce_kernel<M, A, R><<<grid, RED_NT, 0, st>>>(cm, x, gy, y, mean, slope, partial, g_out, bc)
+#define PG_RED_ACTS(M)                          \
+  switch (act) {                                \
+    case ACT_RELU: PG_RED(M, ACT_RELU, false); break;       \
+    case ACT_LRELU: PG_RED(M, ACT_LRELU, false); break;     \
+    case ACT_TANH: PG_RED(M, ACT_TANH, false); break;       \
+    case ACT_SIGMOID: PG_RED(M, ACT_SIGMOID, false); break; \
+    default: PG_RED(M, ACT_NONE, false); break;             \
+  }
+  switch (mode) {
+    case RED_SUM: PG_RED(RED_SUM, ACT_NONE, false); break;
+    case RED_SQDEV: PG_RED(RED_SQDEV, ACT_NONE, false); break;
+    case RED_BN_BWD:
+      if (rec && act == ACT_RELU) PG_RED(RED_BN_BWD, ACT_RELU, true);
+      else if (rec) PG_RED(RED_BN_BWD, ACT_LRELU, true);
+      else PG_RED_ACTS(RED_BN_BWD);
+      break;
+    case RED_ACT_G: PG_RED_ACTS(RED_ACT_G); break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef PG_RED_ACTS
+#undef PG_RED
   return launched();
 }
 

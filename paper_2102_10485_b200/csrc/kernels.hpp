@@ -68,8 +68,8 @@ size_t reduce_partial_floats(const ChannelMap& cm);
 // RED_ACT_G with g_out: also writes g1 = act_bwd(gy, y) (activation backward + bias sums in one pass)
 // BN coefficients of a block (istd [L][Cp], gamma/beta at gb + l gb_ls): given
 // to bn_bwd_apply, it recomputes a ReLU / LeakyReLU output from the pre-BN map
-// instead of reading the stored y (bit-identical, see bn_pre).  Measured: 21%
-// off bn_bwd_apply; the same recompute in channel_reduce made it 9% slower.
+// instead of reading the stored y (bit-identical, see bn_pre); channel_reduce
+// (RED_BN_BWD) does the same when given them.
 struct BnCoef {
   const float* istd = nullptr;
   const float* gb = nullptr;
@@ -77,7 +77,7 @@ struct BnCoef {
 };
 cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x, const float* gy, const float* y,
                                   const float* mean, int act, float slope, float* partial, cudaStream_t st,
-                                  float* g_out = nullptr);
+                                  float* g_out = nullptr, BnCoef bc = {});
 
 // BN forward finalize: pass 0 -> mean; pass 1 -> var, inv_std, running-stat update.
 cudaError_t launch_bn_finalize_mean(const ChannelMap& cm, const float* partial, float* mean, cudaStream_t st);

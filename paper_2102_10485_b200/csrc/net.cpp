@@ -585,8 +585,12 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
         cs.nslot = 1;
         cs.npack = 1;
       } else {
+        static const bool yfree_red = [] {
+          const char* e = std::getenv("PG_YFREE_RED");  // 0: read the stored y (A/B timing)
+          return !(e && e[0] == '0');
+        }();
         check_cuda(launch_channel_reduce(cm, RED_BN_BWD, t.pre[i].p, gy, t.act[i + 1], t.mean[i].p, b.act, b.slope,
-                                         partial_.p, st),
+                                         partial_.p, st, nullptr, yfree_red ? bnc : BnCoef{}),
                    "bn bwd reduce");
       }
       bool closed_form_bias = b.bias_per_bn_channel();
