@@ -276,6 +276,7 @@ __global__ void bn_eval_stats_kernel(ChannelMap cm, const float* running, long l
 // float4 over [L][R][Cp] (Cp % 4 == 0).  When the grid stride is a multiple of
 // the row width (the usual case: Cp / 4 divides 256), each thread keeps one
 // channel group for all its elements and holds its coefficients in registers.
+template <int ACT>
 __global__ void __launch_bounds__(256) bn_apply_kernel(ChannelMap cm, const float* __restrict__ x,
                                                        const float* __restrict__ mean, const float* __restrict__ istd,
                                                        const float* __restrict__ gb, long long gb_ls, int act,
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(ChannelMap cm, const floa
       float o4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        o4[u] = c0 + u < cm.C ? act_fwd(act, bn_pre(a[u], r[u], m[u], bb[u]), slope) : 0.f;
+        o4[u] = c0 + u < cm.C ? act_fwd(ACT, bn_pre(a[u], r[u], m[u], bb[u]), slope) : 0.f;
       return make_float4(o4[0], o4[1], o4[2], o4[3]);
     };
     long long q = q0;
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(ChannelMap cm, const floa
       int c = c0 + u;
       if (c < cm.C) {
         long long mc = (long long)l * cm.Cp + c;
-        r[u] = act_fwd(act, bn_pre(gamma[c] * istd[mc], r[u], mean[mc], beta[c]), slope);
+        r[u] = act_fwd(ACT, bn_pre(gamma[c] * istd[mc], r[u], mean[mc], beta[c]), slope);
       } else {
         r[u] = 0.f;
       }
@@ -471,18 +472,33 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(ChannelMap cm, const 
   }
 }
 
-__global__ void act_bwd_kernel(ChannelMap cm, const float* __restrict__ gy, const float* __restrict__ y, int act,
-                               float slope, float* g) {
+template <int ACT>
+__global__ void __launch_bounds__(256) act_bwd_kernel(ChannelMap cm, const float* __restrict__ gy,
+                                                      const float* __restrict__ y, float slope, float* g) {
   const long long per = (long long)cm.R * cm.Cp / 4;
   const int l = blockIdx.y;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < per; q += (long long)gridDim.x * blockDim.x) {
-    const long long o = (long long)l * cm.ls + q * 4;
-    float4 g4 = *reinterpret_cast<const float4*>(gy + o);
-    float4 y4 = *reinterpret_cast<const float4*>(y + o);
-    float4 r = make_float4(act_bwd(act, g4.x, y4.x, slope), act_bwd(act, g4.y, y4.y, slope),
-                           act_bwd(act, g4.z, y4.z, slope), act_bwd(act, g4.w, y4.w, slope));
-    *reinterpret_cast<float4*>(g + o) = r;
+  const float* gl = gy + (long long)l * cm.ls;
+  const float* yl = y + (long long)l * cm.ls;
+  float* ol = g + (long long)l * cm.ls;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  auto bwd = [&](float4 g4, float4 y4) {
+    return make_float4(act_bwd(ACT, g4.x, y4.x, slope), act_bwd(ACT, g4.y, y4.y, slope),
+                       act_bwd(ACT, g4.z, y4.z, slope), act_bwd(ACT, g4.w, y4.w, slope));
+  };
+  long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; q + 3 * stride < per; q += 4 * stride) {  // four float4 of each map in flight
+    float4 g4[4], y4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      g4[j] = *reinterpret_cast<const float4*>(gl + (q + j * stride) * 4);
+      y4[j] = *reinterpret_cast<const float4*>(yl + (q + j * stride) * 4);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) *reinterpret_cast<float4*>(ol + (q + j * stride) * 4) = bwd(g4[j], y4[j]);
   }
+  for (; q < per; q += stride)
+    *reinterpret_cast<float4*>(ol + q * 4) =
+        bwd(*reinterpret_cast<const float4*>(gl + q * 4), *reinterpret_cast<const float4*>(yl + q * 4));
 }
 
 __global__ void bias_finalize_kernel(ChannelMap cm, const float* partial, float* dbias, long long dbias_ls,
@@ -727,7 +743,15 @@ cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* m
   const long long per = (long long)cm.R * cm.Cp / 4;
   const unsigned cap = std::max(1u, 148u * 8u / (unsigned)std::max(1, cm.L));
   dim3 grid(grid_for(per, 256 * 16, cap), cm.L);
-  bn_apply_kernel<<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y);
+  switch (act) {
+    case ACT_RELU: bn_apply_kernel<ACT_RELU><<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y); break;
+    case ACT_LRELU: bn_apply_kernel<ACT_LRELU><<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y); break;
+    case ACT_TANH: bn_apply_kernel<ACT_TANH><<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y); break;
+    case ACT_SIGMOID:
+      bn_apply_kernel<ACT_SIGMOID><<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y);
+      break;
+    default: bn_apply_kernel<ACT_NONE><<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y); break;
+  }
   return launched();
 }
 
@@ -775,8 +799,16 @@ cudaError_t launch_bn_bwd_apply(const ChannelMap& cm, const float* gy, const flo
 
 cudaError_t launch_act_bwd(const ChannelMap& cm, const float* gy, const float* y, int act, float slope, float* g,
                            cudaStream_t st) {
-  dim3 grid(grid_for((long long)cm.R * cm.Cp / 4, 256, 4096), cm.L);
-  act_bwd_kernel<<<grid, 256, 0, st>>>(cm, gy, y, act, slope, g);
+  const long long per = (long long)cm.R * cm.Cp / 4;
+  const unsigned cap = std::max(1u, 148u * 8u / (unsigned)std::max(1, cm.L));
+  dim3 grid(grid_for(per, 256 * 16, cap), cm.L);
+  switch (act) {
+    case ACT_RELU: act_bwd_kernel<ACT_RELU><<<grid, 256, 0, st>>>(cm, gy, y, slope, g); break;
+    case ACT_LRELU: act_bwd_kernel<ACT_LRELU><<<grid, 256, 0, st>>>(cm, gy, y, slope, g); break;
+    case ACT_TANH: act_bwd_kernel<ACT_TANH><<<grid, 256, 0, st>>>(cm, gy, y, slope, g); break;
+    case ACT_SIGMOID: act_bwd_kernel<ACT_SIGMOID><<<grid, 256, 0, st>>>(cm, gy, y, slope, g); break;
+    default: act_bwd_kernel<ACT_NONE><<<grid, 256, 0, st>>>(cm, gy, y, slope, g); break;
+  }
   return launched();
 }
 
