@@ -377,3 +377,26 @@ def test_cli_train_and_sample_artifacts(tmp_path):
     z = np.load(tmp_path / "s.npz")
     assert z["samples"].shape == (40, 1, 28, 28) and set(np.unique(z["class_ids"])) <= {0, 1, 2}
     assert z["samples"].min() >= 0.0 and z["samples"].max() <= 1.0
+
+
+def test_bn_backward_mask_recompute_is_bit_identical(tmp_path):
+    """The BN-backward kernels take the ReLU / LeakyReLU mask from the pre-BN
+    map and the BN coefficients (elementwise.cu bn_pre) instead of the stored
+    activation output: the recomputed output must be bit-identical to the one
+    bn_apply stored, so whole training runs match byte for byte with the
+    stored-y path (PG_YFREE=0 PG_YFREE_RED=0)."""
+    import os
+    import subprocess
+    import sys
+    outs = []
+    for run, env in (("recompute", {}), ("stored", {"PG_YFREE": "0", "PG_YFREE_RED": "0"})):
+        out = tmp_path / run
+        r = subprocess.run([sys.executable, "-m", "paper_2102_10485_b200", "train", "--arch", "2", "--labels", "2",
+                            "--per-label", "192", "--batch", "64", "--seed", "11", "--out", str(out)],
+                           capture_output=True, text=True, env={**os.environ, **env})
+        assert r.returncode == 0, r.stderr
+        outs.append(out)
+    a, b = outs
+    for k in range(2):
+        assert (a / f"checkpoints/class_{k}.bin").read_bytes() == (b / f"checkpoints/class_{k}.bin").read_bytes()
+    assert (a / "losses.csv").read_text() == (b / "losses.csv").read_text()
