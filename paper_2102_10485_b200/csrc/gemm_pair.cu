@@ -555,6 +555,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
   cluster_sync();  // the peer's barriers exist before anyone arrives remotely
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: everything above touches only parameters, shared memory and TMEM, so
+  // it overlaps the previous kernel's tail; no global data is read before this
+  grid_dep_wait();
+  grid_dep_launch();
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
@@ -920,7 +924,24 @@ cudaError_t launch_pair_st(const CUtensorMap& ta, const CUtensorMap& tb, const P
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gemm_pair_kernel<KIND, BN, MODE, STATS><<<grid, pair_nt(KIND, BN, MODE), smem, st>>>(ta, tb, P);
+  // programmatic dependent launch (PG_PDL=0 turns it off): the prologue runs
+  // while the previous kernel drains (see grid_dep_wait in the kernel)
+  static const bool pdl = [] {
+    const char* e = std::getenv("PG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(pair_nt(KIND, BN, MODE));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_pair_kernel<KIND, BN, MODE, STATS>, ta, tb, P);
+  if (e != cudaSuccess) return e;
   return launched();
 }
 

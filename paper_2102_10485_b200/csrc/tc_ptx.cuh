@@ -152,6 +152,12 @@ PG_DEV void tbox(uint32_t dst, const void* tmap, uint64_t* bar, int c0, int c1, 
   if (PF) tma_pf_5d(tmap, c0, c1, c2, c3, c4); else tma_load_5d(dst, tmap, bar, c0, c1, c2, c3, c4);
 }
 
+// programmatic dependent launch: wait for the preceding grid's completion and
+// memory (no-op when launched without the PDL attribute); allow the next
+// PDL-launched grid to start its prologue
+PG_DEV void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+PG_DEV void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // one lane of the (fully active) warp: the lowest; the same lane every call
 PG_DEV bool elect_one() {
   uint32_t pred = 0;
