@@ -397,7 +397,8 @@ __global__ void dense_fprop_n4_kernel(GemmArgs a) {
   const float* x = a.big + l * a.big_ls + (long long)warp * g.CG;
   const float* w = a.w + l * a.w_ls;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int k = lane * 4; k < g.CG; k += 128) {
+#pragma unroll 4
+  for (int k = lane * 4; k < g.CG; k += 128) {  // unrolled: loads of 4 iterations in flight, same sum order
     const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
 #pragma unroll
     for (int n = 0; n < 4; ++n)
@@ -450,28 +451,32 @@ __global__ void __launch_bounds__(128) dense_fprop_smallk_kernel(GemmArgs a) {
 }
 
 // DGRAD with K = CS <= 4: gx[b][f] = sum_cs gz[b][cs] W[cs][f]
-__global__ void dense_dgrad_k4_kernel(GemmArgs a) {
+__global__ void __launch_bounds__(256) dense_dgrad_k4_kernel(GemmArgs a) {
+  // grid-stride over the float4s of [B][CG/4]: the output write is the whole
+  // cost, so each thread streams several float4 (one per block was
+  // block-scheduling bound at ~1.7 TB/s)
   const ConvGeo& g = a.g;
   const int l = blockIdx.y;
-  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // float4 index over [B][CG/4]
   const int f4n = g.CG / 4;
-  if (q >= (long long)g.B * f4n) return;
-  const int b = (int)(q / f4n), f = (int)(q % f4n) * 4;
-  const float* gz = a.small + l * a.small_ls + (long long)b * g.CS;
+  const long long n = (long long)g.B * f4n;
   const float* w = a.w + l * a.w_ls;
-  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int c = 0; c < g.CS; ++c) {
-    const float gv = gz[c];
-    const float4 wv = __ldg(reinterpret_cast<const float4*>(w + (long long)c * g.CG + f));
-    r.x = fmaf(gv, wv.x, r.x);
-    r.y = fmaf(gv, wv.y, r.y);
-    r.z = fmaf(gv, wv.z, r.z);
-    r.w = fmaf(gv, wv.w, r.w);
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(q / f4n), f = (int)(q % f4n) * 4;
+    const float* gz = a.small + l * a.small_ls + (long long)b * g.CS;
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < g.CS; ++c) {
+      const float gv = gz[c];
+      const float4 wv = __ldg(reinterpret_cast<const float4*>(w + (long long)c * g.CG + f));
+      r.x = fmaf(gv, wv.x, r.x);
+      r.y = fmaf(gv, wv.y, r.y);
+      r.z = fmaf(gv, wv.z, r.z);
+      r.w = fmaf(gv, wv.w, r.w);
+    }
+    float o[4] = {r.x, r.y, r.z, r.w};
+    for (int u = 0; u < 4; ++u)
+      if ((f + u) % a.c_pad >= a.c_valid) o[u] = 0.f;
+    *reinterpret_cast<float4*>(a.out + l * a.out_ls + (long long)b * g.CG + f) = make_float4(o[0], o[1], o[2], o[3]);
   }
-  float o[4] = {r.x, r.y, r.z, r.w};
-  for (int u = 0; u < 4; ++u)
-    if ((f + u) % a.c_pad >= a.c_valid) o[u] = 0.f;
-  *reinterpret_cast<float4*>(a.out + l * a.out_ls + (long long)b * g.CG + f) = make_float4(o[0], o[1], o[2], o[3]);
 }
 
 // WGRAD with M = CS <= 4: dW[cs][f] = sum_b gz[b][cs] x[b][f]
@@ -598,7 +603,8 @@ cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math) {
     }
     case T_D_DGRAD_K4: {
       const long long n = (long long)g.B * (g.CG / 4);
-      dense_dgrad_k4_kernel<<<dim3((unsigned)((n + 255) / 256), a.L), 256, 0, st>>>(a);
+      const long long per_block = 256 * 8;  // eight float4 per thread
+      dense_dgrad_k4_kernel<<<dim3((unsigned)((n + per_block - 1) / per_block), a.L), 256, 0, st>>>(a);
       break;
     }
     case T_D_WGRAD_M4:
