@@ -93,6 +93,7 @@ struct PairPlan {
   const float* stat_mu;
   int stat_act;
   float stat_slope;
+  int blo;  // TF32X3 FPROP: b_lo comes pre-split from global (tmBl) instead of the split warps
 };
 
 // Sum of v[0..7] over the 32 lanes of a warp in 9 shuffles (recursive
@@ -504,7 +505,7 @@ PG_DEV void pair_drain_role(const PairPlan& P, uint32_t tmem, uint64_t* seg_full
 template <int KIND, int BN, int MODE, bool STATS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MODE), 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const PairPlan P) {
+                     const __grid_constant__ CUtensorMap tmBl, const PairPlan P) {
   constexpr bool SPLIT = MODE == MATH_TF32X3;
   constexpr int SH = hi_stages(BN, SPLIT);
   constexpr int SL = lo_stages(BN, SPLIT);
@@ -595,6 +596,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
           const uint32_t b_dst = a_dst + AB;
           pair_issue<KIND, BH>(tmA, tmB, P, a_dst, b_dst, full_h + s, kb, c.label, c.mtp, rank, c.n0, c.b0, c.i0,
                                c.j0, c.d);
+          if (KIND == GEMM_FPROP && SPLIT && P.blo)  // lo slot it % SL == s (equal rings), freed with the hi slot
+            tma_load_3d(smem_u32(lo_base + (it % SL) * SB) + AB, &tmBl, full_h + s, kb * BKT, c.n0, c.label);
           if (PFD > 0) {
             const int kp = kb + PFD;
             if (kp < P.nk)
@@ -623,8 +626,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
           mbar_wait(empty_l + j, ((it / SL) & 1) ^ 1);
           const float4* src = reinterpret_cast<const float4*>(smem + s * SB);
           float4* dst = reinterpret_cast<float4*>(lo_base + j * SB);
+          const int n16 = (KIND == GEMM_FPROP && P.blo ? AB : SB) / 16;  // b_lo already landed by TMA
 #pragma unroll 8
-          for (int i = st; i < SB / 16; i += NSPLIT * 32) {
+          for (int i = st; i < n16; i += NSPLIT * 32) {
             const float4 v = src[i];
             dst[i] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
                                  v.w - tf32_trunc(v.w));
@@ -914,8 +918,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
 // ---------------------------------------------------------------- host side
 
 template <int KIND, int BN, int MODE, bool STATS>
-cudaError_t launch_pair_st(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, int grid,
-                           cudaStream_t st) {
+cudaError_t launch_pair_st(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbl, const PairPlan& P,
+                           int grid, cudaStream_t st) {
   constexpr int smem = smem_total(BN, MODE == MATH_TF32X3);
   static bool configured = false;
   if (!configured) {
@@ -940,7 +944,7 @@ cudaError_t launch_pair_st(const CUtensorMap& ta, const CUtensorMap& tb, const P
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_pair_kernel<KIND, BN, MODE, STATS>, ta, tb, P);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_pair_kernel<KIND, BN, MODE, STATS>, ta, tb, tbl, P);
   if (e != cudaSuccess) return e;
   return launched();
 }
@@ -971,7 +975,8 @@ bool atm_enabled() {
 }
 
 template <int KIND, int BN, int MODE>
-cudaError_t launch_pair_bn(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, cudaStream_t st) {
+cudaError_t launch_pair_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbl, const PairPlan& P,
+                           cudaStream_t st) {
   const int tiles = P.ntn * P.ntmp * P.nz;
   if (tiles == 0 || P.nk == 0) return cudaSuccess;
   const int pairs = std::min(tiles, sm_count_tma() / 2);
@@ -981,16 +986,16 @@ cudaError_t launch_pair_bn(const CUtensorMap& ta, const CUtensorMap& tb, const P
                                       : launch_pair_atm<KIND, BN, false>(ta, tb, P, 2 * pairs, st);
   }
   if (KIND != GEMM_WGRAD && P.stat_mode != STAT_NONE)
-    return launch_pair_st<KIND, BN, MODE, KIND != GEMM_WGRAD>(ta, tb, P, 2 * pairs, st);
-  return launch_pair_st<KIND, BN, MODE, false>(ta, tb, P, 2 * pairs, st);
+    return launch_pair_st<KIND, BN, MODE, KIND != GEMM_WGRAD>(ta, tb, tbl, P, 2 * pairs, st);
+  return launch_pair_st<KIND, BN, MODE, false>(ta, tb, tbl, P, 2 * pairs, st);
 }
 
 template <int KIND, int MODE>
-cudaError_t launch_pair_kind(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, int bn,
-                             cudaStream_t st) {
-  if (bn == 64) return launch_pair_bn<KIND, 64, MODE>(ta, tb, P, st);
-  if (bn == 128) return launch_pair_bn<KIND, 128, MODE>(ta, tb, P, st);
-  return launch_pair_bn<KIND, 256, MODE>(ta, tb, P, st);
+cudaError_t launch_pair_kind(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbl, const PairPlan& P,
+                             int bn, cudaStream_t st) {
+  if (bn == 64) return launch_pair_bn<KIND, 64, MODE>(ta, tb, tbl, P, st);
+  if (bn == 128) return launch_pair_bn<KIND, 128, MODE>(ta, tb, tbl, P, st);
+  return launch_pair_bn<KIND, 256, MODE>(ta, tb, tbl, P, st);
 }
 
 int pair_bn(int n) { return n >= 256 ? 256 : n >= 128 ? 128 : 64; }
@@ -1089,6 +1094,42 @@ int gemm_pair_stat_slots(const GemmArgs& a, int* npack) {
   return g.s * g.s * ((b.nb * b.ny * b.nx + 1) / 2) * 8;
 }
 
+// b_lo of the weights, [L][rows] contiguous (the stride of `w` may be the
+// whole parameter arena): lo = x - trunc_tf32(x), the split warps' formula
+__global__ void tf32_lo_kernel(const float* __restrict__ w, long long w_ls, long long n, float* __restrict__ out) {
+  const int l = blockIdx.y;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float v = w[l * w_ls + i];
+    out[l * n + i] = v - tf32_trunc(v);
+  }
+}
+cudaError_t launch_tf32_lo(const float* w, long long w_ls, long long n, int L, float* out, cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, std::max(1, 148 * 8 / std::max(1, L)));
+  tf32_lo_kernel<<<dim3(blocks, L), 256, 0, st>>>(w, w_ls, n, out);
+  return launched();
+}
+// grow-only buffer for b_lo (not gemm_scratch: the lowered paths hand
+// gemm_scratch pointers to this engine as operands)
+float* blo_buffer(size_t floats, cudaStream_t st) {
+  static float* buf = nullptr;
+  static size_t cap = 0;
+  if (floats > cap) {
+    cudaStreamSynchronize(st);
+    cudaFree(buf);
+    buf = nullptr;
+    if (cudaMalloc(&buf, floats * sizeof(float)) != cudaSuccess) return nullptr;
+    cap = floats;
+  }
+  return buf;
+}
+bool blo_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PG_BLO");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   const ConvGeo& g = a.g;
   PairPlan P{};
@@ -1123,7 +1164,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   }();
   P.kseg = kseg_env > 0 ? kseg_env : 8;
   const int kk = g.k * g.k;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tbl{};
   const int one[5] = {1, 1, 1, 1, 1};
   const int sstr[5] = {1, g.s, g.s, 1, 1};
   bool ok = true;
@@ -1161,6 +1202,19 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
     const long long bs[2] = {K, a.w_ls};
     const int bbox[3] = {BKT, bn / 2, 1};
     ok = ok && make_map(&tb, a.w, 3, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B);
+    // b_lo pre-split once per launch for the narrow (shared-memory-bound) tiles
+    // when the weights are small against the activations (>= 8 output rows per
+    // weight row): the split warps then only touch A (conv2
+    // forward 1.21 -> 1.11 ms; the wide tiles lose more to the extra pass)
+    if (math == MATH_TF32X3 && bn <= 128 && blo_enabled() && (long long)g.B * g.SH * g.SW >= 8LL * g.CS) {
+      float* wl = blo_buffer((size_t)a.L * K * g.CS, st);
+      if (!wl) return cudaErrorMemoryAllocation;
+      cudaError_t e = launch_tf32_lo(a.w, a.w_ls, K * g.CS, a.L, wl, st);
+      if (e != cudaSuccess) return e;
+      const long long ls[2] = {K, K * g.CS};
+      ok = ok && make_map(&tbl, wl, 3, bd, ls, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B);
+      P.blo = 1;
+    }
   } else if (dgrad_packed(a)) {
     P.N = 4 * g.CG;
     P.kcb = g.CS / BKT;
@@ -1220,6 +1274,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   P.nslot = P.phases * P.ntmp * 8;
   P.CGn = a.kind == GEMM_FPROP ? g.CS : g.CG;
   P.stage_tx = (a.kind == GEMM_WGRAD ? BM : P.box.TB * P.box.TH * P.box.TW) * BKT * 4 + (bn / 2) * BKT * 4;
+  if (P.blo) P.stage_tx += (bn / 2) * BKT * 4;
   // profiling aid: PG_FORCE_STATS=1 runs plain FPROP/DGRAD launches with STAT_FWD into a private buffer
   static const bool force_stats = [] {
     const char* e = std::getenv("PG_FORCE_STATS");
@@ -1241,21 +1296,21 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   if (P.stat_mode != STAT_NONE && (!P.stat || P.N % 8 || P.act != ACT_NONE)) return cudaErrorInvalidValue;
   const bool x3 = math != MATH_TF32;
   if (dgrad_packed(a))
-    return x3 ? launch_pair_kind<KIND_DGP, MATH_TF32X3>(ta, tb, P, bn, st)
-              : launch_pair_kind<KIND_DGP, MATH_TF32>(ta, tb, P, bn, st);
+    return x3 ? launch_pair_kind<KIND_DGP, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
+              : launch_pair_kind<KIND_DGP, MATH_TF32>(ta, tb, tbl, P, bn, st);
   if (f4)
-    return x3 ? launch_pair_kind<KIND_F4, MATH_TF32X3>(ta, tb, P, bn, st)
-              : launch_pair_kind<KIND_F4, MATH_TF32>(ta, tb, P, bn, st);
+    return x3 ? launch_pair_kind<KIND_F4, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
+              : launch_pair_kind<KIND_F4, MATH_TF32>(ta, tb, tbl, P, bn, st);
   switch (a.kind) {
     case GEMM_FPROP:
-      return x3 ? launch_pair_kind<GEMM_FPROP, MATH_TF32X3>(ta, tb, P, bn, st)
-                : launch_pair_kind<GEMM_FPROP, MATH_TF32>(ta, tb, P, bn, st);
+      return x3 ? launch_pair_kind<GEMM_FPROP, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
+                : launch_pair_kind<GEMM_FPROP, MATH_TF32>(ta, tb, tbl, P, bn, st);
     case GEMM_DGRAD:
-      return x3 ? launch_pair_kind<GEMM_DGRAD, MATH_TF32X3>(ta, tb, P, bn, st)
-                : launch_pair_kind<GEMM_DGRAD, MATH_TF32>(ta, tb, P, bn, st);
+      return x3 ? launch_pair_kind<GEMM_DGRAD, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
+                : launch_pair_kind<GEMM_DGRAD, MATH_TF32>(ta, tb, tbl, P, bn, st);
     default:
-      return x3 ? launch_pair_kind<GEMM_WGRAD, MATH_TF32X3>(ta, tb, P, bn, st)
-                : launch_pair_kind<GEMM_WGRAD, MATH_TF32>(ta, tb, P, bn, st);
+      return x3 ? launch_pair_kind<GEMM_WGRAD, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
+                : launch_pair_kind<GEMM_WGRAD, MATH_TF32>(ta, tb, tbl, P, bn, st);
   }
 }
 
