@@ -331,7 +331,7 @@ __host__ __device__ constexpr int seg_bufs(int bn) { return 512 / bn > 4 ? 4 : 5
 template <int KIND, int BH, bool PF = false>
 PG_DEV void pair_issue(const CUtensorMap& tmA, const CUtensorMap& tmB, const PairPlan& P, uint32_t a_dst,
                        uint32_t b_dst, uint64_t* bar, int kb, int label, int mtp, uint32_t rank, int n0, int b0,
-                       int i0, int j0, const DgPhase& d) {
+                       int i0, int j0, const DgPhase& d, const CUtensorMap* tmBl = nullptr, uint32_t bl_dst = 0) {
   const ConvGeo& g = P.g;
   if (KIND == KIND_F4) {
     // eight 128-row x 16-byte boxes (one per tap) side by side along K: the
@@ -370,6 +370,10 @@ PG_DEV void pair_issue(const CUtensorMap& tmA, const CUtensorMap& tmB, const Pai
 #pragma unroll
     for (int q = 0; q < BH / 32; ++q)
       tbox<PF>(b_dst + q * (BKT * 128), &tmB, bar, n0 + 32 * q, ki * g.k + kj, c0, label);
+    if (!PF && tmBl != nullptr)  // pre-split b_lo into the lo slot
+#pragma unroll
+      for (int q = 0; q < BH / 32; ++q)
+        tma_load_4d(bl_dst + q * (BKT * 128), tmBl, bar, n0 + 32 * q, ki * g.k + kj, c0, label);
   } else {
     int kb0, ki0, kj0;
     box_origin(P.box, kb, kb0, ki0, kj0);
@@ -595,7 +599,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
           const uint32_t a_dst = smem_u32(smem + s * SB);
           const uint32_t b_dst = a_dst + AB;
           pair_issue<KIND, BH>(tmA, tmB, P, a_dst, b_dst, full_h + s, kb, c.label, c.mtp, rank, c.n0, c.b0, c.i0,
-                               c.j0, c.d);
+                               c.j0, c.d, KIND == GEMM_DGRAD && SPLIT && P.blo ? &tmBl : nullptr,
+                               smem_u32(lo_base + (it % (SL ? SL : 1)) * SB) + AB);
           if (KIND == GEMM_FPROP && SPLIT && P.blo)  // lo slot it % SL == s (equal rings), freed with the hi slot
             tma_load_3d(smem_u32(lo_base + (it % SL) * SB) + AB, &tmBl, full_h + s, kb * BKT, c.n0, c.label);
           if (PFD > 0) {
@@ -626,7 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
           mbar_wait(empty_l + j, ((it / SL) & 1) ^ 1);
           const float4* src = reinterpret_cast<const float4*>(smem + s * SB);
           float4* dst = reinterpret_cast<float4*>(lo_base + j * SB);
-          const int n16 = (KIND == GEMM_FPROP && P.blo ? AB : SB) / 16;  // b_lo already landed by TMA
+          const int n16 = ((KIND == GEMM_FPROP || KIND == GEMM_DGRAD) && P.blo ? AB : SB) / 16;  // b_lo landed by TMA
 #pragma unroll 8
           for (int i = st; i < n16; i += NSPLIT * 32) {
             const float4 v = src[i];
@@ -1249,6 +1254,17 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
     const long long bs[3] = {g.CG, (long long)kk * g.CG, a.w_ls};
     const int bbox[4] = {32, 1, BKT, 1};
     ok = ok && make_map(&tb, a.w, 4, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    // b_lo pre-split for the narrow tiles (as FPROP above)
+    if (math == MATH_TF32X3 && bn <= 128 && blo_enabled() && (long long)g.B * g.GH * g.GW >= 8LL * g.CG) {
+      const long long nw = (long long)g.CS * kk * g.CG;
+      float* wl = blo_buffer((size_t)a.L * nw, st);
+      if (!wl) return cudaErrorMemoryAllocation;
+      cudaError_t e = launch_tf32_lo(a.w, a.w_ls, nw, a.L, wl, st);
+      if (e != cudaSuccess) return e;
+      const long long ls[3] = {g.CG, (long long)kk * g.CG, nw};
+      ok = ok && make_map(&tbl, wl, 4, bd, ls, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+      P.blo = 1;
+    }
   } else {
     P.N = g.CS;
     P.mrows = kk * g.CG;
