@@ -167,8 +167,27 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` run directly (no WORLD_SIZE in the environment):
+    launch N ranks, one per GPU, through torch.distributed.run on 127.0.0.1
+    exactly as the driver would, with NCCL_DEBUG=INFO (INIT) so the rank count
+    NCCL brings up is visible.  Rank 0's JSON line is the output."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -179,8 +198,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2102_10485_b200 import GroupSpec, LabelGroup, _native as N, algorithmic_flops_per_image, baseline_arch

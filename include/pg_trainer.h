@@ -84,6 +84,15 @@ int pg_group_generate(pg_group* g, long n, uint64_t seed, float* out);
 int pg_group_save_checkpoint(pg_group* g, int label_idx, const char* path);
 int pg_group_load_checkpoint(pg_group* g, int label_idx, const char* path);
 int pg_group_mixture_sample(pg_group* g, const double* priors, long n, uint64_t seed, float* out, int* ids);
+/* Parity instrumentation (off by default; costs one small pass per activation
+ * layer when on): record the ReLU / LeakyReLU masks of every step's five
+ * forward passes (G on z1, D on real, D on fake, G on z2, D on fake), each
+ * activation layer as bytes [B][C][H][W] (1 = positive branch, the
+ * reference's x > 0 / x >= 0 at network.cpp:384-391).  A CPU oracle replays
+ * them to compare gradients without activation-kink discontinuities. */
+int pg_group_capture_masks(pg_group* g, int on);
+/* the last step's masks of one label; returns the byte count (out may be NULL) */
+long pg_group_get_masks(pg_group* g, int label_idx, uint8_t* out, long cap);
 /* device time (ms, CUDA events) of the last pg_group_train_steps call */
 float pg_group_last_ms(pg_group* g);
 int pg_group_sync(pg_group* g);

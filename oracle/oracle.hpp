@@ -418,7 +418,26 @@ template <class R>
 struct LayerTrace {
   Tensor<R> input, output, xhat, mask;
   std::vector<R> mean, inv_std;
+  std::vector<uint8_t> amask;  // forced ReLU / LeakyReLU mask (MaskTape), empty = the sign test
 };
+
+// MaskTape — parity instrumentation, not reference behaviour.  When a tape is
+// installed on the calling thread, every train-mode ReLU / LeakyReLU layer
+// takes its mask (1 = positive branch) from the tape, in call order, instead
+// of the sign test of network.cpp:384-391 / 463-470, and counts where the
+// tape disagrees with that sign test ("forced flips").  Used to replay a
+// device step's activation decisions: a pre-activation within rounding of
+// zero may take either branch in any fp32 summation order, and the tape
+// removes that discontinuity so gradients can be compared at 1e-4.
+struct MaskTape {
+  const uint8_t* m = nullptr;
+  long n = 0, at = 0, flips = 0;
+  std::vector<uint8_t>* record = nullptr;  // non-null: record the sign-test masks instead of forcing
+};
+inline MaskTape*& mask_tape() {
+  thread_local MaskTape* t = nullptr;
+  return t;
+}
 
 template <class R>
 struct Trace {
@@ -689,6 +708,30 @@ void check_batch(const Network<R>& net, const Tensor<R>& x) {
                                 shape_str(in));
 }
 
+// ReLU (leaky = false) / LeakyReLU forward with the mask taken from the tape
+template <class R>
+Tensor<R> forced_act(MaskTape& tp, const Tensor<R>& x, bool leaky, R sl, LayerTrace<R>& tr) {
+  Tensor<R> y(x.shape);
+  if (tp.record) {
+    for (long j = 0; j < y.size(); ++j) {
+      const bool on = leaky ? x[j] >= R(0) : x[j] > R(0);
+      tp.record->push_back(on);
+      y[j] = on ? x[j] : (leaky ? x[j] * sl : R(0));
+    }
+    return y;
+  }
+  if (tp.at + x.size() > tp.n) throw std::invalid_argument("mask tape exhausted");
+  tr.amask.assign(tp.m + tp.at, tp.m + tp.at + x.size());
+  for (long j = 0; j < y.size(); ++j) {
+    const bool own = leaky ? x[j] >= R(0) : x[j] > R(0);
+    const bool on = tr.amask[static_cast<size_t>(j)] != 0;
+    tp.flips += own != on;
+    y[j] = on ? x[j] : (leaky ? x[j] * sl : R(0));
+  }
+  tp.at += x.size();
+  return y;
+}
+
 template <class R>
 Tensor<R> run_layer(const Network<R>& net, size_t i, const Tensor<R>& x, Mode mode, Rng* rng, LayerTrace<R>* tr,
                     std::vector<R>* bufs) {
@@ -718,12 +761,15 @@ Tensor<R> run_layer(const Network<R>& net, size_t i, const Tensor<R>& x, Mode mo
     }
     case Kind::ReLU: {
       Tensor<R> y(x.shape);
+      if (MaskTape* tp = mode == Mode::train && tr ? mask_tape() : nullptr)
+        return forced_act(*tp, x, false, R(0), *tr);
       for (long j = 0; j < y.size(); ++j) y[j] = x[j] > R(0) ? x[j] : R(0);
       return y;
     }
     case Kind::LeakyReLU: {
       Tensor<R> y(x.shape);
       R sl = static_cast<R>(l.slope);
+      if (MaskTape* tp = mode == Mode::train && tr ? mask_tape() : nullptr) return forced_act(*tp, x, true, sl, *tr);
       for (long j = 0; j < y.size(); ++j) y[j] = x[j] >= R(0) ? x[j] : x[j] * sl;
       return y;
     }
@@ -803,11 +849,13 @@ Grads<R> backward(const Network<R>& net, Trace<R>& tr, const Tensor<R>& gout) {
         for (long j = 0; j < gx.size(); ++j) gx[j] = tr.mode == Mode::train ? gy[j] * t.mask[j] : gy[j];
         break;
       case Kind::ReLU:
-        for (long j = 0; j < gx.size(); ++j) gx[j] = t.input[j] > R(0) ? gy[j] : R(0);
+        for (long j = 0; j < gx.size(); ++j)
+          gx[j] = (t.amask.empty() ? t.input[j] > R(0) : t.amask[static_cast<size_t>(j)] != 0) ? gy[j] : R(0);
         break;
       case Kind::LeakyReLU: {
         R sl = static_cast<R>(l.slope);
-        for (long j = 0; j < gx.size(); ++j) gx[j] = t.input[j] >= R(0) ? gy[j] : gy[j] * sl;
+        for (long j = 0; j < gx.size(); ++j)
+          gx[j] = (t.amask.empty() ? t.input[j] >= R(0) : t.amask[static_cast<size_t>(j)] != 0) ? gy[j] : gy[j] * sl;
         break;
       }
       case Kind::Tanh:

@@ -21,6 +21,12 @@ struct GroupBase {
   virtual void set(int l, int what, const double* in, long n) = 0;
   virtual void step_inputs(int l, const double* real01, const double* z1, const double* z2, long B, double* rep) = 0;
   virtual int labels() const = 0;
+  // MaskTape for the label's next step (consumed by it); flips of the last taped step
+  virtual void set_masks(int l, const uint8_t* m, long n) = 0;
+  virtual long mask_flips(int l) const = 0;
+  // record the label's next step's own masks instead (read with get_masks)
+  virtual void record_masks(int l) = 0;
+  virtual long get_masks(int l, uint8_t* out, long cap) = 0;
   // mixture_sample (partition.cpp:182-227) over the group's pairs in label order
   virtual void mixture(const double* priors, long n, uint64_t seed, double* out, int* ids) = 0;
 };
@@ -45,7 +51,75 @@ template <class R>
 struct Group : GroupBase {
   Dataset ds;
   std::vector<std::unique_ptr<Worker<R>>> w;
+  std::vector<std::vector<uint8_t>> masks, recorded;
+  std::vector<long> flips;
+  std::vector<char> recording;
   int labels() const override { return static_cast<int>(w.size()); }
+
+  void set_masks(int l, const uint8_t* m, long n) override {
+    masks.resize(w.size());
+    flips.resize(w.size(), 0);
+    masks.at(static_cast<size_t>(l)).assign(m, m + n);
+  }
+  long mask_flips(int l) const override {
+    return static_cast<size_t>(l) < flips.size() ? flips[static_cast<size_t>(l)] : 0;
+  }
+
+  void record_masks(int l) override {
+    recording.resize(w.size(), 0);
+    recorded.resize(w.size());
+    recording.at(static_cast<size_t>(l)) = 1;
+  }
+  long get_masks(int l, uint8_t* out, long cap) override {
+    if (static_cast<size_t>(l) >= recorded.size()) return 0;
+    const auto& r = recorded[static_cast<size_t>(l)];
+    const long n = static_cast<long>(r.size());
+    if (out) {
+      if (cap < n) throw std::invalid_argument("output buffer too small");
+      std::memcpy(out, r.data(), r.size());
+    }
+    return n;
+  }
+
+  // run f() with label i's mask tape installed (if one is set), then check it was used up
+  template <class F>
+  void taped(size_t i, F f) {
+    if (i < recording.size() && recording[i]) {
+      MaskTape tp;
+      recorded[i].clear();
+      tp.record = &recorded[i];
+      mask_tape() = &tp;
+      try {
+        f();
+      } catch (...) {
+        mask_tape() = nullptr;
+        throw;
+      }
+      mask_tape() = nullptr;
+      recording[i] = 0;
+      return;
+    }
+    if (i >= masks.size() || masks[i].empty()) {
+      f();
+      return;
+    }
+    MaskTape tp;
+    tp.m = masks[i].data();
+    tp.n = static_cast<long>(masks[i].size());
+    mask_tape() = &tp;
+    try {
+      f();
+    } catch (...) {
+      mask_tape() = nullptr;
+      throw;
+    }
+    mask_tape() = nullptr;
+    masks[i].clear();
+    flips[i] = tp.flips;
+    if (tp.at != tp.n)
+      throw std::invalid_argument("mask tape length " + std::to_string(tp.n) + " but the step used " +
+                                  std::to_string(tp.at));
+  }
 
   void step(int n, int threads) override {
     std::atomic<size_t> next{0};
@@ -55,7 +129,7 @@ struct Group : GroupBase {
         size_t i = next.fetch_add(1);
         if (i >= w.size()) break;
         try {
-          for (int s = 0; s < n; ++s) w[i]->step(ds);
+          for (int s = 0; s < n; ++s) taped(i, [&] { w[i]->step(ds); });
         } catch (const std::exception& e) {
           errs[i] = e.what();
         }
@@ -105,6 +179,17 @@ struct Group : GroupBase {
       case 1: take(p.disc.params, in, n); return;
       case 2: take(p.gen.buffers, in, n); return;
       case 3: take(p.disc.buffers, in, n); return;
+      case 6: take(p.opt_g.m, in, n); return;
+      case 7: take(p.opt_g.v, in, n); return;
+      case 8: take(p.opt_d.m, in, n); return;
+      case 9: take(p.opt_d.v, in, n); return;
+      case 12:
+        // Adam step counters {t_g, t_d, steps} (pg_group_set COUNTERS)
+        if (n != 3) throw std::invalid_argument("length mismatch on set");
+        p.opt_g.t = static_cast<long>(in[0]);
+        p.opt_d.t = static_cast<long>(in[1]);
+        p.steps = static_cast<long>(in[2]);
+        return;
     }
     throw std::invalid_argument("field not settable: " + std::to_string(what));
   }
@@ -134,7 +219,8 @@ struct Group : GroupBase {
       b[i] = static_cast<R>(z2[i]);
     }
     int calls = 0;
-    StepReport r = step_core<R>(k.pair, real, [&]() { return calls++ == 0 ? a : b; }, k.rng);
+    StepReport r;
+    taped(static_cast<size_t>(l), [&] { r = step_core<R>(k.pair, real, [&]() { return calls++ == 0 ? a : b; }, k.rng); });
     k.reports.push_back(r);
     if (rep) {
       rep[0] = r.j_d;
@@ -267,6 +353,24 @@ int or_group_mixture(void* h, const double* priors, long n, uint64_t seed, doubl
 }
 
 void or_group_destroy(void* h) { delete static_cast<GroupBase*>(h); }
+
+// Parity instrumentation: force the ReLU / LeakyReLU masks of label l's next
+// step (bytes in the order the step evaluates them: G fwd z1, D fwd real,
+// D fwd fake, G fwd z2, D fwd fake; each layer [B][C][H][W]); returns via
+// or_group_mask_flips how many of them disagreed with the oracle's own sign test.
+int or_group_set_masks(void* h, int label_idx, const uint8_t* masks, long n) {
+  return guard([&] { static_cast<GroupBase*>(h)->set_masks(label_idx, masks, n); });
+}
+long or_group_mask_flips(void* h, int label_idx) { return static_cast<GroupBase*>(h)->mask_flips(label_idx); }
+// record the label's next step's own masks (same order); read them with or_group_get_masks
+int or_group_record_masks(void* h, int label_idx) {
+  return guard([&] { static_cast<GroupBase*>(h)->record_masks(label_idx); });
+}
+long or_group_get_masks(void* h, int label_idx, uint8_t* out, long cap) {
+  long n = -1;
+  if (guard([&] { n = static_cast<GroupBase*>(h)->get_masks(label_idx, out, cap); }) != 0) return -1;
+  return n;
+}
 
 // One label of the cosine-field dataset, [per_label][C][H][W] in [0,1].
 int or_dataset_label(long C, long H, long W, int label, long per_label, uint64_t seed, double* out) {

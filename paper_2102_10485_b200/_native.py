@@ -95,6 +95,8 @@ _SIGNATURES = {
     "pg_group_save_checkpoint": (C.c_int, [_P, C.c_int, C.c_char_p]),
     "pg_group_load_checkpoint": (C.c_int, [_P, C.c_int, C.c_char_p]),
     "pg_group_mixture_sample": (C.c_int, [_P, C.POINTER(C.c_double), C.c_long, C.c_uint64, _F, C.POINTER(C.c_int)]),
+    "pg_group_capture_masks": (C.c_int, [_P, C.c_int]),
+    "pg_group_get_masks": (C.c_long, [_P, C.c_int, C.POINTER(C.c_uint8), C.c_long]),
     "pg_group_last_ms": (C.c_float, [_P]),
     "pg_group_sync": (C.c_int, [_P]),
     "pg_group_sizes": (C.c_int, [_P, C.POINTER(C.c_longlong)]),

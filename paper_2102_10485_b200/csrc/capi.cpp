@@ -490,6 +490,12 @@ int pg_group_load_checkpoint(pg_group* g, int label_idx, const char* path) {
 int pg_group_mixture_sample(pg_group* g, const double* priors, long n, uint64_t seed, float* out, int* ids) {
   return WITH_GROUP(grp.mixture_sample(priors, n, seed, out, ids));
 }
+int pg_group_capture_masks(pg_group* g, int on) { return WITH_GROUP(grp.capture_masks(on != 0)); }
+long pg_group_get_masks(pg_group* g, int label_idx, uint8_t* out, long cap) {
+  long n = -1;
+  int rc = WITH_GROUP(n = grp.get_masks(label_idx, out, cap));
+  return rc == PG_OK ? n : rc;
+}
 float pg_group_last_ms(pg_group* g) { return g ? G(g)->g->last_device_ms() : -1.f; }
 int pg_group_sync(pg_group* g) { return WITH_GROUP(grp.sync()); }
 int pg_group_sizes(pg_group* g, long long* out) {

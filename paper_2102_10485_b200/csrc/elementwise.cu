@@ -15,14 +15,17 @@ namespace {
 
 constexpr int RED_NT = 256;
 
-// rows per reduction chunk: 512, halved (down to 32) until the grid has ~8
-// blocks per SM, so the small deep-layer maps (a few hundred rows per label)
+// rows per reduction chunk: 512, halved (down to 32) until every label has
+// ~10 blocks, so the small deep-layer maps (a few hundred rows per label)
 // are not latency bound on a handful of blocks.  A pure function of the map:
 // the reduce kernel and every reader of its partials agree on it.
 __host__ __device__ inline int red_rows(const ChannelMap& cm) {
   const int c4n = cm.Cp / 4, gpb = c4n < RED_NT ? c4n : RED_NT, ny = (c4n + gpb - 1) / gpb;
+  // per-label criterion only (never the label count), so a label's sums round
+  // identically however the labels are grouped (test_grouping_invariance);
+  // < 10 blocks per label reproduces the old whole-grid rule at L = 125
   int rows = 512;
-  while (rows > 32 && (long long)cm.L * ny * ((cm.R + rows - 1) / rows) < 148 * 8) rows >>= 1;
+  while (rows > 32 && ny * ((cm.R + rows - 1) / rows) < 10) rows >>= 1;
   return rows;
 }
 
@@ -891,6 +894,36 @@ cudaError_t launch_nhwc_to_nchw01(long long N, int C, int H, int W, int Cp, cons
 
 cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t st) {
   fill_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(p, n, v);
+  return launched();
+}
+
+// Parity instrumentation (not on the training path unless capture is enabled):
+// the ReLU / LeakyReLU masks of an activation output map y [L][B][H][W][Cp],
+// as bytes in the reference's [B][C][H][W] order, with act_bwd's convention
+// (ReLU: y > 0, LeakyReLU: y >= 0 -- equal to the reference's x > 0 / x >= 0).
+__global__ void mask_capture_kernel(int B, int H, int W, int C, int Cp, long long ls, const float* __restrict__ y,
+                                    int leaky, unsigned char* __restrict__ out, long long out_ls) {
+  const int l = blockIdx.y;
+  const long long per = (long long)B * C * H * W;
+  const float* yl = y + l * ls;
+  unsigned char* ol = out + l * out_ls;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per; i += (long long)gridDim.x * blockDim.x) {
+    long long r = i;
+    const int x = (int)(r % W);
+    r /= W;
+    const int yy = (int)(r % H);
+    r /= H;
+    const int c = (int)(r % C);
+    const long long b = r / C;
+    const float v = yl[((b * H + yy) * W + x) * Cp + c];
+    ol[i] = leaky ? (v >= 0.f) : (v > 0.f);
+  }
+}
+
+cudaError_t launch_mask_capture(int L, int B, int H, int W, int C, int Cp, long long ls, const float* y, int act,
+                                unsigned char* out, long long out_ls, cudaStream_t st) {
+  dim3 grid(grid_for((long long)B * C * H * W, 256, 256), L);
+  mask_capture_kernel<<<grid, 256, 0, st>>>(B, H, W, C, Cp, ls, y, act == ACT_LRELU ? 1 : 0, out, out_ls);
   return launched();
 }
 

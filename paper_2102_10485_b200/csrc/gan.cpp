@@ -1,5 +1,7 @@
 #include "gan.hpp"
 
+#include "device_cache.hpp"
+
 #include <algorithm>
 #include <cstring>
 
@@ -118,13 +120,17 @@ GanGroup::~GanGroup() {
     if (staged_[par]) cudaEventDestroy(staged_[par]);
   }
   cudaFree(d_flags_);
+  if (d_mask_) cudaFree(d_mask_);
   cudaFree(d_t_g_);
   cudaFree(d_t_d_);
   cudaFree(d_rep_);
   cudaFreeHost(h_rep_);
   if (t0_) cudaEventDestroy(t0_);
   if (t1_) cudaEventDestroy(t1_);
-  if (st_) cudaStreamDestroy(st_);
+  if (st_) {
+    release_stream_scratch(st_);
+    cudaStreamDestroy(st_);
+  }
 }
 
 void GanGroup::set_dataset(const float* images01) {
@@ -205,14 +211,18 @@ void GanGroup::enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t 
   const int pstride = static_cast<int>(D_->out_map().Cp);
   const int nbg = G_->blocks(), nbd = D_->blocks();
   double* rep = d_rep_ + (steps_ % rep_cap_) * L_ * 4;
+  long long moff = 0;  // mask capture (parity instrumentation), in the order the passes run
   // discriminator update on (real, fresh fake); the generator trace is dropped
   tg_.act[0] = dz_[par][0].p;
   G_->forward(tg_, B, true, true, st_);
+  if (capture_) moff = capture_pass(*G_, tg_, B, moff);
   tdr_.act[0] = const_cast<float*>(real_nhwc);
   if (real_ready) check_cuda(cudaStreamWaitEvent(st_, real_ready, 0), "wait real batch");
   D_->forward(tdr_, B, true, true, st_);
+  if (capture_) moff = capture_pass(*D_, tdr_, B, moff);
   tdf_.act[0] = tg_.act[static_cast<size_t>(nbg)];
   D_->forward(tdf_, B, true, true, st_);
+  if (capture_) moff = capture_pass(*D_, tdf_, B, moff);
   check_cuda(launch_loss_d(L_, B, tdr_.act[static_cast<size_t>(nbd)], tdf_.act[static_cast<size_t>(nbd)], pstride,
                            cfg_.clamp, gp_real_.p, gp_fake_.p, rep, st_),
              "loss_d");
@@ -227,8 +237,13 @@ void GanGroup::enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t 
   // generator update through the updated discriminator (its grads discarded)
   tg_.act[0] = dz_[par][1].p;
   G_->forward(tg_, B, true, true, st_);
+  if (capture_) moff = capture_pass(*G_, tg_, B, moff);
   tdf_.act[0] = tg_.act[static_cast<size_t>(nbg)];
   D_->forward(tdf_, B, true, true, st_);
+  if (capture_) {
+    moff = capture_pass(*D_, tdf_, B, moff);
+    mask_len_ = moff;
+  }
   check_cuda(launch_loss_g(L_, B, tdf_.act[static_cast<size_t>(nbd)], pstride, cfg_.clamp, gp_fake_.p, rep, st_),
              "loss_g");
   D_->backward(tdf_, B, gp_fake_.p, false, false, gimg_.p, st_);
@@ -242,6 +257,52 @@ void GanGroup::enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t 
   steps_ += 1;
   pending_ += 1;
   if (pending_ >= rep_cap_) drain_reports();
+}
+
+static long long act_mask_bytes(const DevNet& net, int B) {
+  long long n = 0;
+  for (int i = 0; i < net.blocks(); ++i) {
+    const Block& b = net.block(i);
+    if (b.act == ACT_RELU || b.act == ACT_LRELU) n += static_cast<long long>(B) * b.out.C * b.out.H * b.out.W;
+  }
+  return n;
+}
+
+void GanGroup::capture_masks(bool on) {
+  sync();
+  capture_ = on;
+  mask_len_ = 0;
+  if (on && !d_mask_) {
+    const int Bmax = static_cast<int>(std::min<long>(cfg_.batch, cfg_.per_label));
+    mask_stride_ = 2 * act_mask_bytes(*G_, Bmax) + 3 * act_mask_bytes(*D_, Bmax);
+    d_mask_ = dev_alloc<unsigned char>(static_cast<size_t>(L_) * std::max<long long>(mask_stride_, 1));
+  }
+}
+
+long long GanGroup::capture_pass(DevNet& net, Trace& t, int B, long long off) {
+  for (int i = 0; i < net.blocks(); ++i) {
+    const Block& b = net.block(i);
+    if (b.act != ACT_RELU && b.act != ACT_LRELU) continue;
+    check_cuda(launch_mask_capture(L_, B, static_cast<int>(b.out.H), static_cast<int>(b.out.W),
+                                   static_cast<int>(b.out.C), static_cast<int>(b.out.Cp),
+                                   static_cast<long long>(B) * b.out.numel(), t.act[static_cast<size_t>(i) + 1], b.act,
+                                   d_mask_ + off, mask_stride_, st_),
+               "mask capture");
+    off += static_cast<long long>(B) * b.out.C * b.out.H * b.out.W;
+  }
+  return off;
+}
+
+long GanGroup::get_masks(int label, unsigned char* out, long cap) {
+  if (label < 0 || label >= L_) throw std::out_of_range("label index " + std::to_string(label));
+  sync();
+  if (out && mask_len_ > 0) {
+    if (cap < mask_len_) throw std::invalid_argument("output buffer too small");
+    check_cuda(cudaMemcpy(out, d_mask_ + static_cast<size_t>(label) * mask_stride_, static_cast<size_t>(mask_len_),
+                          cudaMemcpyDeviceToHost),
+               "masks D2H");
+  }
+  return static_cast<long>(mask_len_);
 }
 
 void GanGroup::drain_reports() {

@@ -81,6 +81,14 @@ class GanGroup {
   void sync();
   long steps_done() const { return steps_; }
 
+  // Parity instrumentation: when on, every step records the ReLU / LeakyReLU
+  // masks of its five forward passes (G z1, D real, D fake, G z2, D fake; each
+  // activation layer [B][C][H][W] in the reference's order) so a CPU oracle can
+  // replay the same activation decisions (oracle MaskTape).  Off by default.
+  void capture_masks(bool on);
+  // bytes of the last step's masks for one label (out may be null to query)
+  long get_masks(int label, unsigned char* out, long cap);
+
   // time of the last train_steps() call on the device (ms, CUDA events)
   float last_device_ms() const { return last_ms_; }
 
@@ -117,6 +125,12 @@ class GanGroup {
   std::vector<std::vector<StepReport>> reports_;
   float last_ms_ = 0.f;
   long zcp_ = 0;  // padded latent width
+
+  bool capture_ = false;
+  unsigned char* d_mask_ = nullptr;
+  long long mask_stride_ = 0;  // bytes per label
+  long long mask_len_ = 0;     // bytes per label used by the last step
+  long long capture_pass(DevNet& net, Trace& t, int B, long long off);
 
   int next_batch_size() const;
   void prep_host(int par, int B, bool with_idx);

@@ -6,7 +6,9 @@
 #include <string>
 #include <mutex>
 #include <vector>
+#include <map>
 
+#include "device_cache.hpp"
 #include "kernels.hpp"
 
 namespace pg {
@@ -50,25 +52,63 @@ std::string gemm_timing_report() {
   return out;
 }
 
-// grow-only device scratch shared by the split-K paths (stream-ordered users)
-float* gemm_scratch(size_t floats, cudaStream_t st) {
-  static float* buf = nullptr;
-  static size_t cap = 0;
-  std::lock_guard<std::mutex> g(g_mu);
-  if (floats > cap) {
-    if (buf) {
+// grow-only device scratch per (device, stream, slot): the split-K paths
+// (SCRATCH_GEMM) and the pair engine's pre-split weight lo parts (SCRATCH_BLO;
+// a separate slot because the lowered paths hand SCRATCH_GEMM pointers to that
+// engine as operands)
+namespace {
+struct ScratchKey {
+  int dev;
+  cudaStream_t st;
+  int slot;
+  bool operator<(const ScratchKey& o) const {
+    if (dev != o.dev) return dev < o.dev;
+    if (st != o.st) return st < o.st;
+    return slot < o.slot;
+  }
+};
+struct ScratchBuf {
+  float* p = nullptr;
+  size_t cap = 0;
+};
+std::mutex g_scratch_mu;
+std::map<ScratchKey, ScratchBuf> g_scratch;
+}  // namespace
+
+float* stream_scratch(int slot, size_t floats, cudaStream_t st) {
+  std::lock_guard<std::mutex> g(g_scratch_mu);
+  ScratchBuf& b = g_scratch[ScratchKey{cur_device(), st, slot}];
+  if (floats > b.cap) {
+    if (b.p) {
       cudaStreamSynchronize(st);
-      cudaFree(buf);
+      cudaFree(b.p);
     }
-    buf = nullptr;
-    if (cudaMalloc(&buf, floats * sizeof(float)) != cudaSuccess) {
-      cap = 0;
+    b.p = nullptr;
+    b.cap = 0;
+    if (cudaMalloc(&b.p, floats * sizeof(float)) != cudaSuccess) {
+      b.p = nullptr;
       return nullptr;
     }
-    cap = floats;
+    b.cap = floats;
   }
-  return buf;
+  return b.p;
 }
+
+void release_stream_scratch(cudaStream_t st) {
+  std::lock_guard<std::mutex> g(g_scratch_mu);
+  const int dev = cur_device();
+  for (auto it = g_scratch.begin(); it != g_scratch.end();) {
+    if (it->first.st == st && it->first.dev == dev) {
+      cudaStreamSynchronize(st);
+      cudaFree(it->second.p);
+      it = g_scratch.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+float* gemm_scratch(size_t floats, cudaStream_t st) { return stream_scratch(SCRATCH_GEMM, floats, st); }
 
 cudaError_t launched() {
   g_launches.fetch_add(1, std::memory_order_relaxed);

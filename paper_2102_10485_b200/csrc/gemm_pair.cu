@@ -30,6 +30,7 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include "device_cache.hpp"
 #include "kernels.hpp"
 #include "tc_ptx.cuh"
 #include "tma_common.cuh"
@@ -926,13 +927,12 @@ template <int KIND, int BN, int MODE, bool STATS>
 cudaError_t launch_pair_st(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbl, const PairPlan& P,
                            int grid, cudaStream_t st) {
   constexpr int smem = smem_total(BN, MODE == MATH_TF32X3);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel<KIND, BN, MODE, STATS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static PerDeviceOnce configured;
+  cudaError_t ce = configured.run([&] {
+    return cudaFuncSetAttribute(gemm_pair_kernel<KIND, BN, MODE, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem);
+  });
+  if (ce != cudaSuccess) return ce;
   // programmatic dependent launch (PG_PDL=0 turns it off): the prologue runs
   // while the previous kernel drains (see grid_dep_wait in the kernel)
   static const bool pdl = [] {
@@ -958,13 +958,12 @@ template <int KIND, int BN, bool STATS>
 cudaError_t launch_pair_atm(const CUtensorMap& ta, const CUtensorMap& tb, const PairPlan& P, int grid,
                             cudaStream_t st) {
   constexpr int smem = atm_smem(BN);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_pair_atm_kernel<KIND, BN, STATS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static PerDeviceOnce configured;
+  cudaError_t ce = configured.run([&] {
+    return cudaFuncSetAttribute(gemm_pair_atm_kernel<KIND, BN, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem);
+  });
+  if (ce != cudaSuccess) return ce;
   gemm_pair_atm_kernel<KIND, BN, STATS><<<grid, ATM_NT, smem, st>>>(ta, tb, P);
   return launched();
 }
@@ -1115,18 +1114,7 @@ cudaError_t launch_tf32_lo(const float* w, long long w_ls, long long n, int L, f
 }
 // grow-only buffer for b_lo (not gemm_scratch: the lowered paths hand
 // gemm_scratch pointers to this engine as operands)
-float* blo_buffer(size_t floats, cudaStream_t st) {
-  static float* buf = nullptr;
-  static size_t cap = 0;
-  if (floats > cap) {
-    cudaStreamSynchronize(st);
-    cudaFree(buf);
-    buf = nullptr;
-    if (cudaMalloc(&buf, floats * sizeof(float)) != cudaSuccess) return nullptr;
-    cap = floats;
-  }
-  return buf;
-}
+float* blo_buffer(size_t floats, cudaStream_t st) { return stream_scratch(SCRATCH_BLO, floats, st); }
 bool blo_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PG_BLO");

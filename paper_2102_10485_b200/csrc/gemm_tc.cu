@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "device_cache.hpp"
 #include "gemm_gather.cuh"
 #include "tc_ptx.cuh"
 #include "kernels.hpp"
@@ -502,13 +503,11 @@ int sm_count() {
 template <int KIND, int BN, int MODE>
 cudaError_t launch_bn(const GemmArgs& a, cudaStream_t st) {
   constexpr int smem = smem_bytes(BN, MODE == MATH_TF32X3);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_tc_kernel<KIND, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static PerDeviceOnce configured;
+  cudaError_t ce = configured.run([&] {
+    return cudaFuncSetAttribute(gemm_tc_kernel<KIND, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  if (ce != cudaSuccess) return ce;
   TileGrid tg{(gemm_n(a) + BN - 1) / BN, (gemm_max_m(a) + BM - 1) / BM, a.L * gemm_phases(a)};
   if (tg.total() == 0) return cudaSuccess;
   const int grid = std::min(tg.total(), sm_count());
@@ -544,13 +543,12 @@ bool gemm_tc_supported(const GemmArgs& a) {
 }
 
 cudaError_t launch_gemm_tc(const GemmArgs& a, int math, cudaStream_t st) {
-  static bool dbg_set = false;
-  if (!dbg_set) {
+  static PerDeviceOnce dbg_set;  // __constant__ memory is per device
+  dbg_set.run([] {
     const char* e = std::getenv("PG_TC_DEBUG");
     int v = e ? std::atoi(e) : 0;
-    cudaMemcpyToSymbol(c_dbg, &v, sizeof(int));
-    dbg_set = true;
-  }
+    return cudaMemcpyToSymbol(c_dbg, &v, sizeof(int));
+  });
   if (math == MATH_TF32) return launch_mode<MATH_TF32>(a, st);
   return launch_mode<MATH_TF32X3>(a, st);
 }

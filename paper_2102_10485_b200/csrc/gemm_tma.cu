@@ -33,6 +33,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "device_cache.hpp"
 #include "gemm_gather.cuh"
 #include "tma_common.cuh"
 #include "kernels.hpp"
@@ -362,13 +363,11 @@ __global__ void __launch_bounds__(NT, 1)
 template <int KIND, int BN, int MODE>
 cudaError_t launch_tma_bn(const CUtensorMap& ta, const CUtensorMap& tb, const TmaPlan& P, cudaStream_t st) {
   constexpr int smem = smem_total(BN, MODE == MATH_TF32X3);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_tma_kernel<KIND, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static PerDeviceOnce configured;
+  cudaError_t ce = configured.run([&] {
+    return cudaFuncSetAttribute(gemm_tma_kernel<KIND, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  if (ce != cudaSuccess) return ce;
   const int tiles = P.ntn * P.ntm * P.nz;
   if (tiles == 0 || P.nk == 0) return cudaSuccess;
   const int grid = std::min(tiles, sm_count_tma());

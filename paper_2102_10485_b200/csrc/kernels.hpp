@@ -138,5 +138,9 @@ cudaError_t launch_nchw01_to_nhwc(long long N, int C, int H, int W, int Cp, cons
 cudaError_t launch_nhwc_to_nchw01(long long N, int C, int H, int W, int Cp, const float* in, float* out,
                                   cudaStream_t st);
 cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t st);
+// parity instrumentation: ReLU / LeakyReLU masks of y [L][B][H][W][Cp] as bytes
+// out[l * out_ls + ((b C + c) H + h) W + w] (reference NCHW order)
+cudaError_t launch_mask_capture(int L, int B, int H, int W, int C, int Cp, long long ls, const float* y, int act,
+                                unsigned char* out, long long out_ls, cudaStream_t st);
 
 }  // namespace pg

@@ -15,6 +15,7 @@
 //                   K <= 4 and WGRAD with M <= 4 (outer products)
 #include <algorithm>
 
+#include "device_cache.hpp"
 #include "gemm_gather.cuh"
 #include "kernels.hpp"
 
@@ -550,12 +551,12 @@ cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math) {
       const int kk = g.k * g.k;
       const size_t smem = sizeof(float4) * g.CS * kk +
                           sizeof(float) * od_patch(OD_TY, g.k, g.s) * od_patch(OD_TX, g.k, g.s) * (g.CS + 4);
-      static size_t configured = 0;
-      if (smem > 48 * 1024 && smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(thin_out_dgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+      static PerDeviceMax configured;
+      if (smem > 48 * 1024) {
+        cudaError_t e = configured.raise(smem, [&] {
+          return cudaFuncSetAttribute(thin_out_dgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        });
         if (e != cudaSuccess) return e;
-        configured = smem;
       }
       const unsigned tiles = (unsigned)(((g.GW + OD_TX - 1) / OD_TX) * ((g.GH + OD_TY - 1) / OD_TY));
       thin_out_dgrad_kernel<<<dim3(tiles, g.B, a.L), OD_THREADS, smem, st>>>(a);
@@ -565,12 +566,12 @@ cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math) {
       const int TJ = std::min(pow2ceil_thin(g.SW), IF_PIX), TI = IF_PIX / TJ;
       const int kk = g.k * g.k;
       const size_t smem = sizeof(float4) * (64 * kk + ((TI - 1) * g.s + g.k) * ((TJ - 1) * g.s + g.k));
-      static size_t configured = 0;
-      if (smem > 48 * 1024 && smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(thin_in_fprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+      static PerDeviceMax configured;
+      if (smem > 48 * 1024) {
+        cudaError_t e = configured.raise(smem, [&] {
+          return cudaFuncSetAttribute(thin_in_fprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        });
         if (e != cudaSuccess) return e;
-        configured = smem;
       }
       const unsigned tiles = (unsigned)(((g.SW + TJ - 1) / TJ) * ((g.SH + TI - 1) / TI));
       thin_in_fprop_kernel<<<dim3(tiles, g.B, a.L), IF_THREADS, smem, st>>>(a, TI, TJ);

@@ -181,6 +181,21 @@ class LabelGroup:
                                                 _fptr(out), ids.ctypes.data_as(C.POINTER(C.c_int))), "mixture_sample")
         return out, ids
 
+    def capture_masks(self, on: bool = True) -> None:
+        """Parity instrumentation: record every step's ReLU / LeakyReLU masks
+        (pg_group_capture_masks)."""
+        N.check(N.lib().pg_group_capture_masks(self._h, 1 if on else 0), "capture_masks")
+
+    def masks(self, label_index: int) -> np.ndarray:
+        """the last step's masks of one label, bytes in the oracle MaskTape order"""
+        L = N.lib()
+        n = N.check(L.pg_group_get_masks(self._h, label_index, None, 0), "get_masks")
+        out = np.zeros(n, np.uint8)
+        if n:
+            N.check(L.pg_group_get_masks(self._h, label_index, out.ctypes.data_as(C.POINTER(C.c_uint8)), n),
+                    "get_masks")
+        return out
+
     def sizes(self) -> dict:
         out = (C.c_longlong * 4)()
         N.check(N.lib().pg_group_sizes(self._h, out), "sizes")

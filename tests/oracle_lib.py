@@ -47,6 +47,12 @@ def lib() -> C.CDLL:
                                      D, D, D, D]
         h.or_net_info.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_long)]
         h.or_net_init.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.c_double, D]
+        h.or_group_set_masks.argtypes = [P, C.c_int, C.POINTER(C.c_uint8), C.c_long]
+        h.or_group_mask_flips.restype = C.c_long
+        h.or_group_mask_flips.argtypes = [P, C.c_int]
+        h.or_group_record_masks.argtypes = [P, C.c_int]
+        h.or_group_get_masks.restype = C.c_long
+        h.or_group_get_masks.argtypes = [P, C.c_int, C.POINTER(C.c_uint8), C.c_long]
         h.or_bench_steps.restype = C.c_double
         h.or_bench_steps.argtypes = [C.c_int, C.c_int, C.c_int, C.c_long, C.c_int, C.c_int]
         _lib = h
@@ -90,6 +96,28 @@ class OracleGroup:
     def set(self, label: int, what: int, v: np.ndarray) -> None:
         v = np.ascontiguousarray(v, np.float64)
         check(lib().or_group_set(self.h, label, what, _d(v), v.size))
+
+    def set_masks(self, label: int, masks: np.ndarray) -> None:
+        """Force the ReLU / LeakyReLU masks of the label's next step (MaskTape,
+        oracle.hpp): bytes in the order the step evaluates them."""
+        m = np.ascontiguousarray(masks, np.uint8)
+        self._keep = m
+        check(lib().or_group_set_masks(self.h, label, m.ctypes.data_as(C.POINTER(C.c_uint8)), m.size))
+
+    def mask_flips(self, label: int) -> int:
+        """elements of the last taped step where the forced mask disagreed with the oracle's sign test"""
+        return int(lib().or_group_mask_flips(self.h, label))
+
+    def record_masks(self, label: int) -> None:
+        """record the label's next step's own ReLU / LeakyReLU masks (MaskTape order)"""
+        check(lib().or_group_record_masks(self.h, label))
+
+    def recorded_masks(self, label: int) -> np.ndarray:
+        n = lib().or_group_get_masks(self.h, label, None, 0)
+        out = np.zeros(max(n, 0), np.uint8)
+        if n > 0:
+            lib().or_group_get_masks(self.h, label, out.ctypes.data_as(C.POINTER(C.c_uint8)), n)
+        return out
 
     def mixture(self, priors, n: int, seed: int, sample_shape) -> tuple[np.ndarray, np.ndarray]:
         """mixture_sample (partition.cpp:182-227) over the group's pairs: samples in [0,1], class indices."""

@@ -87,3 +87,17 @@ def layer_tensors(spec: str, in_shape: tuple) -> list[tuple[str, int, int, bool]
             out += [(f"{i}.bn.gamma", off, c, False), (f"{i}.bn.beta", off + c, c, False)]
             off += 2 * c
     return out
+
+
+def update_err(p_new: np.ndarray, p_ref_new: np.ndarray, p_old: np.ndarray) -> float:
+    """Error of an optimizer update (p_new - p_old vs p_ref_new - p_old) in
+    units of the bar: max over elements of |du - dr| / (max|dr| + ulp32),
+    i.e. relative to the largest reference update, with the fp32 rounding of
+    the stored weight itself (one ulp of p_ref_new in float32) added to the
+    allowance -- an fp32 parameter near 1 (BN gamma) cannot hold a 1e-4
+    update to better than ~1e-3 of itself."""
+    du = np.asarray(p_new, np.float64) - p_old
+    dr = np.asarray(p_ref_new, np.float64) - p_old
+    scale = max(np.abs(dr).max(initial=0.0), 1e-30)
+    ulp = np.spacing(np.abs(p_ref_new).astype(np.float32)).astype(np.float64)
+    return float((np.abs(du - dr) / (scale + ulp / 1e-4)).max(initial=0.0))
