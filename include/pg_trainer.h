@@ -44,6 +44,8 @@ typedef struct {
   int math;               /* PG_MATH_* */
   int threads;            /* host threads for per-label RNG work */
   int device;             /* CUDA device ordinal */
+  const uint64_t* seeds;  /* optional [n_labels] worker seeds (WorkerConfig::seed, partition.hpp:34);
+                             NULL: derive_seed(base_seed, class_id) */
 } pg_group_config;
 
 /* Fields for pg_group_get / pg_group_set (reference layouts, f64). */
@@ -74,6 +76,8 @@ int pg_group_set(pg_group* g, int label_index, int field, const double* in, long
 int pg_group_failed(pg_group* g, int* failed);
 /* eval-mode samples for every label: latents from Rng(derive_seed(seed, class_id)); out [n_labels][n][C][H][W] in [0,1] */
 int pg_group_generate(pg_group* g, long n, uint64_t seed, float* out);
+/* generate (gan.cpp:197-201) on caller-drawn latents z [n_labels][n][d_z]: out [n_labels][n][C][H][W] in [0,1] */
+int pg_group_generate_latents(pg_group* g, const float* z, long n, float* out);
 /* mixture_sample (include/partgan/partition.hpp, src/partition.cpp:182-227) over the
  * group's labels in order: priors[n_labels]; class ids then per-class latents drawn
  * from Rng(seed) exactly as the reference; out [n][C][H][W] in [0,1], ids[n] */

@@ -38,6 +38,7 @@ class GroupConfig(C.Structure):
         ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
         ("clamp", C.c_double), ("init_std", C.c_double),
         ("math", C.c_int), ("threads", C.c_int), ("device", C.c_int),
+        ("seeds", C.POINTER(C.c_uint64)),
     ]
 
 
@@ -86,6 +87,22 @@ _SIGNATURES = {
     "pg_group_set": (C.c_int, [_P, C.c_int, C.c_int, _D, C.c_long]),
     "pg_group_failed": (C.c_int, [_P, _I]),
     "pg_group_generate": (C.c_int, [_P, C.c_long, C.c_uint64, _F]),
+    "pg_group_generate_latents": (C.c_int, [_P, _F, C.c_long, _F]),
+    "pg_net_create": (C.c_int, [C.c_char_p, C.POINTER(C.c_long), C.c_int, C.c_uint64, C.c_double, C.c_int, C.c_int,
+                                C.POINTER(_P)]),
+    "pg_net_destroy": (None, [_P]),
+    "pg_net_param_count": (C.c_long, [_P]),
+    "pg_net_buffer_count": (C.c_long, [_P]),
+    "pg_net_out_shape": (C.c_int, [_P, C.POINTER(C.c_long), _I]),
+    "pg_net_get_params": (C.c_int, [_P, _D]),
+    "pg_net_set_params": (C.c_int, [_P, _D]),
+    "pg_net_get_buffers": (C.c_int, [_P, _D]),
+    "pg_net_set_buffers": (C.c_int, [_P, _D]),
+    "pg_net_forward": (C.c_int, [_P, _D, C.c_int, C.c_int, _D, C.POINTER(_P)]),
+    "pg_net_backward": (C.c_int, [_P, _P, _D, C.c_int, _D, _D]),
+    "pg_trace_destroy": (None, [_P]),
+    "pg_adam_step_host": (C.c_int, [C.c_long, _D, _D, _D, _D, C.POINTER(C.c_long), C.c_double, C.c_double,
+                                    C.c_double, C.c_double, C.c_int]),
     "pg_softmax_rows": (C.c_int, [C.POINTER(C.c_double), C.c_long, C.c_long, C.POINTER(C.c_double)]),
     "pg_inception_score": (C.c_int, [C.POINTER(C.c_double), C.c_long, C.c_long, C.c_int, C.POINTER(C.c_double),
                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -3,9 +3,14 @@
 #include <string>
 
 #include "../../include/pg_trainer.h"
+#include "capi_util.hpp"
 #include "gan.hpp"
 
 namespace pg {
+std::string& last_error() {
+  thread_local std::string e;
+  return e;
+}
 void softmax_rows(const double* logits, long n, long k, double* probs);
 void inception_score(const double* probs, long n, long k, int n_splits, double* split_scores, double* mean,
                      double* stddev);
@@ -15,24 +20,7 @@ void anova_per_channel(const float* images, const int* labels, long n, long C, l
 
 namespace {
 
-thread_local std::string g_err;
-
-template <class F>
-int guard(F f) {
-  try {
-    f();
-    return PG_OK;
-  } catch (const std::invalid_argument& e) {
-    g_err = e.what();
-    return PG_EINVAL;
-  } catch (const std::out_of_range& e) {
-    g_err = e.what();
-    return PG_EINVAL;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return PG_ECUDA;
-  }
-}
+using pg::guard;
 
 void cuda_ok(cudaError_t e, const char* what) { pg::check_cuda(e, what); }
 
@@ -99,7 +87,7 @@ Group* G(pg_group* p) { return reinterpret_cast<Group*>(p); }
 
 extern "C" {
 
-const char* pg_last_error(void) { return g_err.c_str(); }
+const char* pg_last_error(void) { return pg::last_error().c_str(); }
 
 int pg_device_count(void) {
   int n = 0;
@@ -430,6 +418,7 @@ int pg_group_create(const pg_group_config* c, pg_group** out) {
     cfg.init_std = c->init_std;
     cfg.math = c->math;
     cfg.threads = c->threads;
+    if (c->seeds) cfg.seeds.assign(c->seeds, c->seeds + c->n_labels);
     auto grp = std::make_unique<Group>();
     grp->device = c->device;
     grp->g = std::make_unique<pg::GanGroup>(cfg);
@@ -481,6 +470,9 @@ int pg_group_failed(pg_group* g, int* failed) {
   });
 }
 int pg_group_generate(pg_group* g, long n, uint64_t seed, float* out) { return WITH_GROUP(grp.generate(n, seed, out)); }
+int pg_group_generate_latents(pg_group* g, const float* z, long n, float* out) {
+  return WITH_GROUP(grp.generate_latents(z, n, out));
+}
 int pg_group_save_checkpoint(pg_group* g, int label_idx, const char* path) {
   return WITH_GROUP(pg::save_checkpoint(grp, label_idx, path));
 }

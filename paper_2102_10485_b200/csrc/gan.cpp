@@ -22,7 +22,7 @@ T* dev_alloc(size_t n) {
   check_cuda(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)), "cudaMemset");
   return static_cast<T*>(p);
 }
-std::string shape3(long C, long H, long W) {
+[[maybe_unused]] std::string shape3(long C, long H, long W) {
   return std::to_string(C) + " " + std::to_string(H) + " " + std::to_string(W);
 }
 }  // namespace
@@ -39,11 +39,16 @@ GanGroup::GanGroup(const GroupConfig& cfg) : cfg_(cfg), L_(static_cast<int>(cfg.
   D_ = std::make_unique<DevNet>(cfg_.disc_spec, std::vector<long>{cfg_.C, cfg_.H, cfg_.W}, L_, Bmax, cfg_.math);
   // make_gan_pair shape checks (gan.cpp:41-48)
   std::vector<long> img{cfg_.C, cfg_.H, cfg_.W};
+  auto sstr = [](const std::vector<long>& v) {
+    std::string r = "[";
+    for (size_t i = 0; i < v.size(); ++i) r += (i ? "x" : "") + std::to_string(v[i]);
+    return r + "]";
+  };
   if (G_->ref_out_shape() != img)
-    throw std::invalid_argument("generator emits a shape that does not match images " + shape3(cfg_.C, cfg_.H, cfg_.W));
+    throw std::invalid_argument("generator emits " + sstr(G_->ref_out_shape()) + " but images are " + sstr(img));
   long dout = 1;
   for (long d : D_->ref_out_shape()) dout *= d;
-  if (dout != 1) throw std::invalid_argument("discriminator must emit a scalar");
+  if (dout != 1) throw std::invalid_argument("discriminator must emit a scalar, got " + sstr(D_->ref_out_shape()));
 
   check_cuda(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&cst_, cudaStreamNonBlocking), "copy stream");
@@ -80,8 +85,11 @@ GanGroup::GanGroup(const GroupConfig& cfg) : cfg_(cfg), L_(static_cast<int>(cfg.
   std::vector<float> gp(static_cast<size_t>(L_) * G_->P()), dp(static_cast<size_t>(L_) * D_->P());
   std::vector<float> gb(static_cast<size_t>(L_) * std::max<long long>(G_->Bf(), 4), 0.f),
       db(static_cast<size_t>(L_) * std::max<long long>(D_->Bf(), 4), 0.f);
+  if (!cfg_.seeds.empty() && static_cast<int>(cfg_.seeds.size()) != L_)
+    throw std::invalid_argument("GanGroup: " + std::to_string(cfg_.seeds.size()) + " worker seeds for " +
+                                std::to_string(L_) + " labels");
   pool_->parallel_for(L_, [&](int l) {
-    uint64_t wseed = derive_seed(cfg_.base_seed, static_cast<uint64_t>(cfg_.class_ids[static_cast<size_t>(l)]));
+    uint64_t wseed = worker_seed(l);
     auto g = G_->init_ref_params(derive_seed(wseed, 1), cfg_.init_std);
     auto d = D_->init_ref_params(derive_seed(wseed, 2), cfg_.init_std);
     G_->import_params(g.data(), gp.data() + static_cast<size_t>(l) * G_->P());
@@ -97,13 +105,19 @@ GanGroup::GanGroup(const GroupConfig& cfg) : cfg_(cfg), L_(static_cast<int>(cfg.
 
   // run_worker: Rng rng(cfg.seed) per label; order = the label's shard
   rng_.reserve(static_cast<size_t>(L_));
-  for (int l = 0; l < L_; ++l)
-    rng_.emplace_back(derive_seed(cfg_.base_seed, static_cast<uint64_t>(cfg_.class_ids[static_cast<size_t>(l)])));
+  for (int l = 0; l < L_; ++l) rng_.emplace_back(worker_seed(l));
   order_.assign(static_cast<size_t>(L_), std::vector<int>(static_cast<size_t>(cfg_.per_label)));
   for (auto& o : order_)
     for (long j = 0; j < cfg_.per_label; ++j) o[static_cast<size_t>(j)] = static_cast<int>(j);
   last_batch_.assign(static_cast<size_t>(L_), {});
   reports_.assign(static_cast<size_t>(L_), {});
+}
+
+// run_worker: Rng rng(cfg.seed), make_gan_pair(..., cfg.seed) (partition.cpp:85-87) with
+// cfg.seed = derive_seed(base_seed, class_id) (run.cpp:376) unless given per label
+uint64_t GanGroup::worker_seed(int l) const {
+  if (!cfg_.seeds.empty()) return cfg_.seeds[static_cast<size_t>(l)];
+  return derive_seed(cfg_.base_seed, static_cast<uint64_t>(cfg_.class_ids[static_cast<size_t>(l)]));
 }
 
 GanGroup::~GanGroup() {
@@ -530,21 +544,18 @@ void GanGroup::set(int label, int what, const double* in, long n) {
   throw std::invalid_argument("field not settable: " + std::to_string(what));
 }
 
-void GanGroup::generate(long n, uint64_t seed, float* out) {
+// eval-mode generator over all labels in rounds of up to Bmax samples;
+// fill_z(l, B, done, z) writes label l's B latents (padded rows of zcp_)
+void GanGroup::generate_rounds(long n, const std::function<void(int, int, long, float*)>& fill_z, float* out) {
   sync();
   const int Bmax = static_cast<int>(std::min<long>(cfg_.batch, cfg_.per_label));
   const Map& om = G_->out_map();
-  std::vector<Rng> rs;
-  for (int l = 0; l < L_; ++l) rs.emplace_back(derive_seed(seed, static_cast<uint64_t>(cfg_.class_ids[static_cast<size_t>(l)])));
-  DeviceBuf o(static_cast<size_t>(L_) * Bmax * cfg_.C * cfg_.H * cfg_.W);
+  const long S = cfg_.C * cfg_.H * cfg_.W;
+  DeviceBuf o(static_cast<size_t>(L_) * Bmax * S);
   std::vector<float> zh(static_cast<size_t>(L_) * Bmax * zcp_, 0.f), oh(o.n);
   for (long done = 0; done < n; done += Bmax) {
-    int B = static_cast<int>(std::min<long>(Bmax, n - done));
-    pool_->parallel_for(L_, [&](int l) {
-      for (int b = 0; b < B; ++b)
-        for (long j = 0; j < cfg_.d_z; ++j)
-          zh[(static_cast<size_t>(l) * B + b) * zcp_ + j] = static_cast<float>(rs[static_cast<size_t>(l)].normal());
-    });
+    const int B = static_cast<int>(std::min<long>(Bmax, n - done));
+    pool_->parallel_for(L_, [&](int l) { fill_z(l, B, done, zh.data() + static_cast<size_t>(l) * B * zcp_); });
     check_cuda(cudaMemcpyAsync(dz_[0][0].p, zh.data(), sizeof(float) * L_ * B * zcp_, cudaMemcpyHostToDevice, st_), "z");
     tg_.act[0] = dz_[0][0].p;
     G_->forward(tg_, B, false, false, st_);
@@ -552,15 +563,30 @@ void GanGroup::generate(long n, uint64_t seed, float* out) {
                                      static_cast<int>(cfg_.W), static_cast<int>(om.Cp),
                                      tg_.act[static_cast<size_t>(G_->blocks())], o.p, st_),
                "to nchw");
-    check_cuda(cudaMemcpyAsync(oh.data(), o.p, sizeof(float) * L_ * B * cfg_.C * cfg_.H * cfg_.W,
-                               cudaMemcpyDeviceToHost, st_),
-               "samples D2H");
+    check_cuda(cudaMemcpyAsync(oh.data(), o.p, sizeof(float) * L_ * B * S, cudaMemcpyDeviceToHost, st_), "samples D2H");
     check_cuda(cudaStreamSynchronize(st_), "sync");
-    const long S = cfg_.C * cfg_.H * cfg_.W;
     for (int l = 0; l < L_; ++l)
       std::memcpy(out + (static_cast<size_t>(l) * n + done) * S, oh.data() + static_cast<size_t>(l) * B * S,
                   sizeof(float) * B * S);
   }
+}
+
+void GanGroup::generate(long n, uint64_t seed, float* out) {
+  std::vector<Rng> rs;
+  for (int l = 0; l < L_; ++l) rs.emplace_back(derive_seed(seed, static_cast<uint64_t>(cfg_.class_ids[static_cast<size_t>(l)])));
+  generate_rounds(n, [&](int l, int B, long, float* z) {
+    for (int b = 0; b < B; ++b)
+      for (long j = 0; j < zcp_; ++j) z[b * zcp_ + j] = j < cfg_.d_z ? static_cast<float>(rs[static_cast<size_t>(l)].normal()) : 0.f;
+  }, out);
+}
+
+void GanGroup::generate_latents(const float* zin, long n, float* out) {
+  if (n < 1) throw std::invalid_argument("generate: n must be >= 1");
+  generate_rounds(n, [&](int l, int B, long done, float* z) {
+    for (int b = 0; b < B; ++b)
+      for (long j = 0; j < zcp_; ++j)
+        z[b * zcp_ + j] = j < cfg_.d_z ? zin[(static_cast<size_t>(l) * n + done + b) * cfg_.d_z + j] : 0.f;
+  }, out);
 }
 
 void GanGroup::mixture_sample(const double* priors, long n, uint64_t seed, float* out, int* ids) {

@@ -12,6 +12,7 @@
 // Labels never exchange data; grouping changes the launch shape, not the math.
 #pragma once
 
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -28,6 +29,7 @@ struct GroupConfig {
   long d_z = 100;
   std::vector<int> class_ids;  // labels of this group
   uint64_t base_seed = 1;      // worker seed = derive_seed(base_seed, class_id)  (run.cpp:376)
+  std::vector<uint64_t> seeds; // explicit per-label worker seeds (WorkerConfig::seed); overrides base_seed
   int batch = 64;
   int epochs = 1;
   long per_label = 64;         // shard size of every label
@@ -74,6 +76,8 @@ class GanGroup {
   // eval-mode samples: n per label with latents from Rng(derive_seed(seed, class_id)),
   // (v+1)/2 mapped, out [L][n][C][H][W]
   void generate(long n, uint64_t seed, float* out);
+  // eval-mode samples from given latents z [L][n][d_z] (generate's device half), out [L][n][C][H][W]
+  void generate_latents(const float* z, long n, float* out);
   // mixture_sample (partition.cpp:182-227) over the group's labels in order:
   // class ids and latents drawn on the host from Rng(seed) in the reference
   // order, eval-mode generators on the device; out [n][C][H][W] in [0,1]
@@ -132,6 +136,8 @@ class GanGroup {
   long long mask_len_ = 0;     // bytes per label used by the last step
   long long capture_pass(DevNet& net, Trace& t, int B, long long off);
 
+  uint64_t worker_seed(int l) const;
+  void generate_rounds(long n, const std::function<void(int, int, long, float*)>& fill_z, float* out);
   int next_batch_size() const;
   void prep_host(int par, int B, bool with_idx);
   void enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t real_ready = nullptr);

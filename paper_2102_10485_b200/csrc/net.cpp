@@ -503,6 +503,7 @@ GemmArgs DevNet::linear_args(const Block& b, int B, const float* x, float* y, bo
 
 void DevNet::forward(Trace& t, int B, bool train, bool update_running, cudaStream_t st) {
   if (B < 1 || B > Bmax_) throw std::invalid_argument("batch size outside [1, max_batch]");
+  t.train = train;
   for (size_t i = 0; i < blocks_.size(); ++i) {
     const Block& b = blocks_[i];
     if (!b.has_bn) {
@@ -596,7 +597,8 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
       bool closed_form_bias = b.bias_per_bn_channel();
       check_cuda(launch_bn_bwd_finalize(cs, partial_.p, t.istd[i].p, params.p + b.off_bn, P_,
                                         param_grads ? grads.p + b.off_bn : nullptr, P_,
-                                        closed_form_bias ? dbias : nullptr, P_, accumulate ? 1 : 0, 1, coef_.p, st),
+                                        closed_form_bias ? dbias : nullptr, P_, accumulate ? 1 : 0, t.train ? 1 : 0,
+                                        coef_.p, st),
                  "bn bwd finalize");
       bias_done = closed_form_bias;
       check_cuda(launch_bn_bwd_apply(cm, gy, t.act[i + 1], t.pre[i].p, t.mean[i].p, coef_.p, fused ? ACT_NONE : b.act,

@@ -90,6 +90,7 @@ struct Trace {
   std::vector<DeviceBuf> own;   // owned activation buffers (index i >= 1)
   std::vector<DeviceBuf> pre;   // pre-BatchNorm linear output per block (BN blocks)
   std::vector<DeviceBuf> mean, istd;
+  bool train = true;  // mode of the forward that filled it (backward's BatchNorm form)
 };
 
 class DevNet {
