@@ -27,6 +27,14 @@ bool lowered_enabled(const GemmArgs& a) {
   }();
   return !(off & (a.kind == GEMM_FPROP ? 1 : 2));
 }
+// PG_DENSE_WIDE=0: the wide dense layers on the previous engines (A/B timing)
+bool dense_wide_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PG_DENSE_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 // FPROP shapes the SIMT thin kernels also accept but the pair engine runs
 // faster: the 4-channel image side (direct TMA gather, KIND_F4) and wide dense
 // layers with a small K (the generator's latent projection, K = 100)
@@ -143,6 +151,7 @@ double gemm_timing_read_ms() {
 int gemm_stat_slots(const GemmArgs& a, int math, int* npack) {
   if (npack) *npack = 1;
   if (math == MATH_FP32_SIMT) return 0;
+  if (dense_wide_enabled() && dense_wide_supported(a)) return dense_wide_stat_slots(a);
   if (lowered_enabled(a) && gemm_lowered_supported(a)) return gemm_lowered_stat_slots(a);
   if (image_side_direct(a)) return gemm_pair_stat_slots(a, npack);
   if (gemm_thin_supported(a)) return 0;
@@ -158,7 +167,8 @@ cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
     cudaEventRecord(e0, st);
   }
   cudaError_t r;
-  if (math != MATH_FP32_SIMT && lowered_enabled(a) && gemm_lowered_supported(a)) r = launch_gemm_lowered(a, math, st);
+  if (dense_wide_enabled() && dense_wide_supported(a)) r = launch_dense_wide(a, st);  // latent projection
+  else if (math != MATH_FP32_SIMT && lowered_enabled(a) && gemm_lowered_supported(a)) r = launch_gemm_lowered(a, math, st);
   else if (math != MATH_FP32_SIMT && image_side_direct(a)) r = launch_gemm_pair(a, math, st);  // 4-channel FPROP
   else if (gemm_thin_supported(a)) r = launch_gemm_thin(a, st, math);  // image-side / dense-head shapes
   else if (math != MATH_FP32_SIMT && gemm_pair_supported(a)) r = launch_gemm_pair(a, math, st);  // big conv GEMMs

@@ -34,6 +34,10 @@ bool gemm_pair_supported(const GemmArgs& a);
 cudaError_t launch_gemm_lowered(const GemmArgs& a, int math, cudaStream_t st);  // im2col / col2im + pair engine
 bool gemm_lowered_supported(const GemmArgs& a);
 int gemm_pair_stat_slots(const GemmArgs& a, int* npack = nullptr);
+// dense_wide.cu: wide dense FPROP with K <= 256 (the generator's latent projection), fp32 FMA
+bool dense_wide_supported(const GemmArgs& a);
+int dense_wide_stat_slots(const GemmArgs& a);
+cudaError_t launch_dense_wide(const GemmArgs& a, cudaStream_t st);
 int gemm_lowered_stat_slots(const GemmArgs& a);
 // number of 32-row statistic slots launch_gemm(a, math) writes when a.stat_mode
 // is set (0: the engine chosen for this GEMM cannot fuse statistics); *npack =
