@@ -3,6 +3,7 @@
 #include "device_cache.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace pg {
@@ -78,6 +79,11 @@ GanGroup::GanGroup(const GroupConfig& cfg) : cfg_(cfg), L_(static_cast<int>(cfg.
   d_t_d_ = dev_alloc<long long>(static_cast<size_t>(L_));
   rep_cap_ = 256;
   d_rep_ = dev_alloc<double>(static_cast<size_t>(rep_cap_) * L_ * 4);
+  d_rep_cur_ = dev_alloc<double>(static_cast<size_t>(L_) * 4);
+  {
+    const char* e = std::getenv("PG_GRAPH");
+    use_graph_ = !(e && e[0] == '0');
+  }
   h_rep_ = pinned<double>(static_cast<size_t>(rep_cap_) * L_ * 4);
   pool_ = std::make_unique<ThreadPool>(std::max(1, cfg_.threads));
 
@@ -138,6 +144,9 @@ GanGroup::~GanGroup() {
   cudaFree(d_t_g_);
   cudaFree(d_t_d_);
   cudaFree(d_rep_);
+  cudaFree(d_rep_cur_);
+  for (auto& sg : graphs_)
+    if (sg.exec) cudaGraphExecDestroy(sg.exec);
   cudaFreeHost(h_rep_);
   if (t0_) cudaEventDestroy(t0_);
   if (t1_) cudaEventDestroy(t1_);
@@ -222,9 +231,16 @@ void GanGroup::prep_host(int par, int B, bool with_idx) {
 
 // The adversarial step (gan.cpp:136-176) for all labels, on st_.
 void GanGroup::enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t real_ready) {
+  enqueue_step_kernels(B, real_nhwc, par, real_ready, d_rep_ + (steps_ % rep_cap_) * L_ * 4);
+  steps_ += 1;
+  pending_ += 1;
+  if (pending_ >= rep_cap_) drain_reports();
+}
+
+// The kernels of one step (gan.cpp:136-176), enqueued on st_; reports to rep.
+void GanGroup::enqueue_step_kernels(int B, const float* real_nhwc, int par, cudaEvent_t real_ready, double* rep) {
   const int pstride = static_cast<int>(D_->out_map().Cp);
   const int nbg = G_->blocks(), nbd = D_->blocks();
-  double* rep = d_rep_ + (steps_ % rep_cap_) * L_ * 4;
   long long moff = 0;  // mask capture (parity instrumentation), in the order the passes run
   // discriminator update on (real, fresh fake); the generator trace is dropped
   tg_.act[0] = dz_[par][0].p;
@@ -268,9 +284,47 @@ void GanGroup::enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t 
                          static_cast<float>(cfg_.lr), cfg_.beta1, cfg_.beta2,
                          static_cast<float>(cfg_.eps), st_),
              "adam G");
+}
+
+// One step of the device-resident worker protocol as a CUDA graph (the real
+// batch gather and every kernel of the step), captured per (staging slot,
+// batch size) once that batch size has run eagerly (so every grow-only buffer
+// has its final size) and replayed afterwards: the c1 / c2 steps are a few
+// hundred short kernels, launch-latency bound without it.  PG_GRAPH=0 (read at
+// group creation) keeps the eager path.
+bool GanGroup::launch_step_graph(int B, int par) {
+  if (!use_graph_ || capture_ || B != graph_B_ready_ || gemm_timing_on()) return false;
+  StepGraph& sg = graphs_[par];
+  if (!sg.exec || sg.B != B) {
+    if (sg.exec) {
+      cudaGraphExecDestroy(sg.exec);
+      sg.exec = nullptr;
+    }
+    const Map& im = D_->in_map();
+    cudaGraph_t graph = nullptr;
+    const long long n0 = launch_count();
+    check_cuda(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "begin capture");
+    check_cuda(launch_gather_real(L_, B, d_idx_[par], data_.p, static_cast<long long>(cfg_.per_label) * im.numel(),
+                                  im.numel(), static_cast<int>(im.Cp), static_cast<int>(im.C), real_.p, st_),
+               "gather");
+    enqueue_step_kernels(B, real_.p, par, nullptr, d_rep_cur_);
+    check_cuda(cudaStreamEndCapture(st_, &graph), "end capture");
+    const cudaError_t e = cudaGraphInstantiate(&sg.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    check_cuda(e, "graph instantiate");
+    sg.B = B;
+    sg.kernels = launch_count() - n0;
+  } else {
+    add_launches(sg.kernels);  // pg_launch_count counts the replayed kernels (bench.py gpu_launches)
+  }
+  check_cuda(cudaGraphLaunch(sg.exec, st_), "graph launch");
+  check_cuda(cudaMemcpyAsync(d_rep_ + (steps_ % rep_cap_) * L_ * 4, d_rep_cur_, sizeof(double) * L_ * 4,
+                             cudaMemcpyDeviceToDevice, st_),
+             "reports");
   steps_ += 1;
   pending_ += 1;
   if (pending_ >= rep_cap_) drain_reports();
+  return true;
 }
 
 static long long act_mask_bytes(const DevNet& net, int B) {
@@ -285,6 +339,7 @@ static long long act_mask_bytes(const DevNet& net, int B) {
 void GanGroup::capture_masks(bool on) {
   sync();
   capture_ = on;
+  graph_B_ready_ = 0;
   mask_len_ = 0;
   if (on && !d_mask_) {
     const int Bmax = static_cast<int>(std::min<long>(cfg_.batch, cfg_.per_label));
@@ -350,10 +405,13 @@ int GanGroup::train_steps(int n) {
                                cudaMemcpyHostToDevice, st_),
                "z2 H2D");
     check_cuda(cudaEventRecord(staged_[par], st_), "event");
-    check_cuda(launch_gather_real(L_, B, d_idx_[par], data_.p, static_cast<long long>(cfg_.per_label) * im.numel(),
-                                  im.numel(), static_cast<int>(im.Cp), static_cast<int>(im.C), real_.p, st_),
-               "gather");
-    enqueue_step(B, real_.p, par);
+    if (!launch_step_graph(B, par)) {
+      check_cuda(launch_gather_real(L_, B, d_idx_[par], data_.p, static_cast<long long>(cfg_.per_label) * im.numel(),
+                                    im.numel(), static_cast<int>(im.Cp), static_cast<int>(im.C), real_.p, st_),
+                 "gather");
+      enqueue_step(B, real_.p, par);
+      if (!capture_) graph_B_ready_ = B;  // buffers now sized for B: later steps of this size may be captured
+    }
     ++done;
   }
   check_cuda(cudaEventRecord(t1_, st_), "event");

@@ -141,6 +141,17 @@ class GanGroup {
   int next_batch_size() const;
   void prep_host(int par, int B, bool with_idx);
   void enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t real_ready = nullptr);
+  void enqueue_step_kernels(int B, const float* real_nhwc, int par, cudaEvent_t real_ready, double* rep);
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    int B = 0;
+    long long kernels = 0;
+  };
+  StepGraph graphs_[2];
+  bool use_graph_ = true;
+  int graph_B_ready_ = 0;        // batch size whose buffers are grown (eager step done)
+  double* d_rep_cur_ = nullptr;  // the graph's report slot (copied into the ring after each replay)
+  bool launch_step_graph(int B, int par);
   void stage_real_async(const float* real01, int B);
   void drain_reports();
 };

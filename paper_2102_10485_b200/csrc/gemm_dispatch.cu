@@ -124,6 +124,8 @@ cudaError_t launched() {
 }
 
 long long launch_count() { return g_launches.load(); }
+void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+bool gemm_timing_on() { return g_timing.load(); }
 
 void gemm_timing_enable(bool on) {
   std::lock_guard<std::mutex> g(g_mu);

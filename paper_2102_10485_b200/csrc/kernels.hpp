@@ -12,6 +12,8 @@ enum MathMode : int { MATH_FP32_SIMT = 0, MATH_TF32X3 = 1, MATH_TF32 = 2 };
 // (bench.py's gpu_launches) and returns the launch status
 cudaError_t launched();
 long long launch_count();
+void add_launches(long long n);  // kernels replayed inside a CUDA graph
+bool gemm_timing_on();
 // optional per-GEMM timing (CUDA events on the launching stream)
 void gemm_timing_enable(bool on);
 double gemm_timing_read_ms();

@@ -494,3 +494,27 @@ def test_grouping_invariance(math):
         for f in fields:
             a, b = whole.get(label, f), part.get(idx, f)
             assert a.tobytes() == b.tobytes(), (label, f)
+
+
+def test_cuda_graph_step_is_bit_identical(monkeypatch):
+    """train_steps replays each step as a CUDA graph once its batch size has
+    run eagerly (c1 / c2 are launch-latency bound).  The replayed steps --
+    including the partial tail batch of an epoch and the next epoch's
+    shuffle -- must equal the eager path (PG_GRAPH=0) byte for byte, and
+    pg_launch_count must keep counting the replayed kernels."""
+    arch = baseline_arch(1)
+    spec = dict(arch=arch, class_ids=[0, 1, 2], batch=16, per_label=40, epochs=2, base_seed=7, math=1)
+    runs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PG_GRAPH", mode)
+        g = LabelGroup(GroupSpec(**spec))
+        g.generate_dataset(3)
+        n0 = N.lib().pg_launch_count()
+        assert g.train_steps(6) == 6  # 16 + 16 + 8 per epoch
+        runs[mode] = (g, N.lib().pg_launch_count() - n0)
+    (eager, n_eager), (graph, n_graph) = runs["0"], runs["1"]
+    assert n_graph == n_eager, (n_graph, n_eager)
+    for label in range(3):
+        for f in (N.F_GEN_PARAMS, N.F_DISC_PARAMS, N.F_GEN_BUFFERS, N.F_DISC_BUFFERS, N.F_GEN_GRADS, N.F_DISC_GRADS,
+                  N.F_GEN_ADAM_M, N.F_DISC_ADAM_V, N.F_REPORTS, N.F_LAST_BATCH, N.F_COUNTERS):
+            assert eager.get(label, f).tobytes() == graph.get(label, f).tobytes(), (label, f)
