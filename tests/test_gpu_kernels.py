@@ -341,9 +341,10 @@ def test_adam_matches_formula_and_rejects_nonfinite(native, torch_cuda):
         for l in range(L):
             if l == 1 and step >= 3:
                 continue
-            b1f, b2f, one = np.float32(b1), np.float32(b2), np.float32(1)
-            m[l] = b1f * m[l] + (one - b1f) * g[l]
-            v[l] = b2f * v[l] + (one - b2f) * g[l] * g[l]
+            # 1 - beta formed in f64 and rounded once (the kernel's ob1 / ob2)
+            b1f, b2f, ob1, ob2 = np.float32(b1), np.float32(b2), np.float32(1 - b1), np.float32(1 - b2)
+            m[l] = b1f * m[l] + ob1 * g[l]
+            v[l] = b2f * v[l] + ob2 * g[l] * g[l]
             c1, c2 = np.float32(1 - b1 ** step), np.float32(1 - b2 ** step)
             p[l] = p[l] - np.float32(lr) * (m[l] / c1) / (np.sqrt(v[l] / c2) + np.float32(eps))
     assert host(f_d).tolist() == [0, 1, 0]
