@@ -254,12 +254,19 @@ def main():
     imgs = world * Lg * args.batch * ran
     value = imgs / (max_ms / 1000.0)
 
-    # per-kernel timing pass (separate from the headline): implicit-GEMM share
+    # per-kernel timing pass (separate from the headline): implicit-GEMM share,
+    # per-layer tensor classes and per-kernel HBM classes (CUDA events around
+    # every launch of one step)
     lib.pg_kernel_timing(1)
     grp.train_steps(1)
     grp.sync()
     gemm_ms = C_double_out(lib.pg_kernel_timing_read)
+    import ctypes as C
+    n_rep = lib.pg_kernel_timing_report(None, 0)
+    rep_buf = C.create_string_buffer(n_rep + 1)
+    lib.pg_kernel_timing_report(rep_buf, n_rep + 1)
     lib.pg_kernel_timing(0)
+    timing_lines = rep_buf.value.decode().splitlines()
     flops_img = algorithmic_flops_per_image(arch)
     step_flops = Lg * args.batch * flops_img
     peaks = measured_peaks()
@@ -277,6 +284,7 @@ def main():
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get("gemm_dram_bytes_per_step")
+    tensor_classes, hbm_classes = kernel_classes(timing_lines, tf32_peak, peaks["hbm_gbs"])
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                 "frac": (achieved / tf32_peak) if achieved else None, "traffic": traffic,
                 "traffic_unit": "bytes per step (all implicit-GEMM launches, ncu dram__bytes_read + write)",
@@ -287,7 +295,13 @@ def main():
                               "back to back on every SM pair)",
                 "bf16_dense_driver": peaks["bf16_tflops"],
                 "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / (max_ms / ran) if ran else None,
-                "algorithmic_flop_per_image": flops_img}
+                "algorithmic_flop_per_image": flops_img,
+                # per GEMM shape (all launches of one step): algorithmic TFLOP/s (padded channel
+                # counts, e.g. RGB as 4) and its fraction of the tf32 peak; pipe_frac = 3x for 3xTF32
+                "tensor_classes": tensor_classes,
+                # HBM-bound kernels: algorithmic bytes / time vs the measured copy bandwidth
+                "hbm_classes": hbm_classes, "hbm_peak_gbs": peaks["hbm_gbs"],
+                "hbm_peak_basis": "MEASURED_PEAKS.json hbm_gbs (" + peaks["source"] + ")"}
 
     # e2e through the public API: host batch (pinned) -> train_step -> reports
     e2e = None
@@ -348,6 +362,38 @@ def main():
     grp.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def kernel_classes(lines, tf32_peak, hbm_gbs):
+    """Aggregate the per-launch timing report of one step: implicit GEMMs by
+    shape (algorithmic FLOP = 2 L M N K x phases), HBM-bound kernels by name
+    (tag bytes = algorithmic bytes moved)."""
+    gemm, hbm = {}, {}
+    for line in lines:
+        parts = line.split()
+        if not parts:
+            continue
+        ms = float(parts[-1])
+        kv = dict(x.split("=", 1) for x in parts[1:-1] if "=" in x)
+        if parts[0] == "hbm":
+            c = hbm.setdefault(parts[1], [0, 0.0, 0.0])
+            c[0] += 1
+            c[1] += ms
+            c[2] += float(kv.get("bytes", 0))
+        else:
+            key = f"{parts[0]} M={kv['M']} N={kv['N']} K={kv['K']}" + (f" x{kv['phases']}" if kv.get("phases", "1") != "1" else "")
+            flops = 2.0 * int(kv["L"]) * int(kv["M"]) * int(kv["N"]) * int(kv["K"]) * int(kv.get("phases", 1))
+            c = gemm.setdefault(key, [0, 0.0, 0.0])
+            c[0] += 1
+            c[1] += ms
+            c[2] += flops
+    tc = [{"class": k, "launches": n, "ms_per_step": ms, "tflops": f / ms / 1e9 if ms else None,
+           "frac": f / ms / 1e9 / tf32_peak if ms else None} for k, (n, ms, f) in gemm.items()]
+    hc = [{"class": k, "launches": n, "ms_per_step": ms, "gbs": b / ms / 1e6 if ms else None,
+           "frac": b / ms / 1e6 / hbm_gbs if ms else None} for k, (n, ms, b) in hbm.items()]
+    tc.sort(key=lambda r: -r["ms_per_step"])
+    hc.sort(key=lambda r: -r["ms_per_step"])
+    return tc, hc
 
 
 def C_double_out(fn) -> float:

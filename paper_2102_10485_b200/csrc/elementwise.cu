@@ -701,6 +701,7 @@ size_t reduce_partial_floats(const ChannelMap& cm) { return (size_t)cm.L * ((cm.
 cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x, const float* gy, const float* y,
                                   const float* mean, int act, float slope, float* partial, cudaStream_t st,
                                   float* g_out, BnCoef bc) {
+  cudaEvent_t t0_ = timing_start(st);
   if (cm.Cp % 4) return cudaErrorInvalidValue;
   const int c4n = cm.Cp / 4, gpb = c4n < RED_NT ? c4n : RED_NT;
   dim3 grid(reduce_chunks(cm), (c4n + gpb - 1) / gpb, cm.L);
@@ -727,7 +728,9 @@ cudaError_t launch_channel_reduce(const ChannelMap& cm, int mode, const float* x
   }
 #undef PG_RED_ACTS
 #undef PG_RED
-  return launched();
+  cudaError_t r_ = launched();
+  timing_stop(t0_, st, "hbm channel_reduce bytes=" + std::to_string((long long)((long long)cm.L * cm.R * cm.Cp * (mode == RED_ACT_G ? 12 : mode == RED_BN_BWD ? (rec ? 8 : 12) : 4))));
+  return r_;
 }
 
 cudaError_t launch_bn_finalize_mean(const ChannelMap& cm, const float* partial, float* mean, cudaStream_t st) {
@@ -754,6 +757,7 @@ cudaError_t launch_bn_eval_stats(const ChannelMap& cm, const float* running, lon
 
 cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* mean, const float* istd,
                             const float* gamma_beta, long long gb_ls, int act, float slope, float* y, cudaStream_t st) {
+  cudaEvent_t t0_ = timing_start(st);
   // few fat threads: each keeps its channel coefficients in registers and
   // streams ~16 float4 (8 blocks per SM over all labels)
   const long long per = (long long)cm.R * cm.Cp / 4;
@@ -768,7 +772,9 @@ cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* m
       break;
     default: bn_apply_kernel<ACT_NONE><<<grid, 256, 0, st>>>(cm, x, mean, istd, gamma_beta, gb_ls, act, slope, y); break;
   }
-  return launched();
+  cudaError_t r_ = launched();
+  timing_stop(t0_, st, "hbm bn_apply bytes=" + std::to_string((long long)(8LL * cm.L * cm.R * cm.Cp)));
+  return r_;
 }
 
 // lanes per channel: about 8 entries per lane, 4..32 (few entries: small blocks)
@@ -806,15 +812,19 @@ cudaError_t launch_bn_bwd_finalize(const ChannelMap& cm, const float* partial, c
 cudaError_t launch_bn_bwd_apply(const ChannelMap& cm, const float* gy, const float* y, const float* x,
                                 const float* mean, const float* coef, int act, float slope, float* gz,
                                 cudaStream_t st, BnCoef bc) {
+  cudaEvent_t t0_ = timing_start(st);
   const long long per = (long long)cm.R * cm.Cp / 4;
   const unsigned cap = std::max(1u, 148u * 8u / (unsigned)std::max(1, cm.L));
   dim3 grid(grid_for(per, 256 * 16, cap), cm.L);
   bn_bwd_apply_kernel<<<grid, 256, 0, st>>>(cm, gy, y, x, mean, coef, act, slope, gz, bc);
-  return launched();
+  cudaError_t r_ = launched();
+  timing_stop(t0_, st, "hbm bn_bwd_apply bytes=" + std::to_string((long long)((bc.istd ? 12LL : 16LL) * cm.L * cm.R * cm.Cp)));
+  return r_;
 }
 
 cudaError_t launch_act_bwd(const ChannelMap& cm, const float* gy, const float* y, int act, float slope, float* g,
                            cudaStream_t st) {
+  cudaEvent_t t0_ = timing_start(st);
   const long long per = (long long)cm.R * cm.Cp / 4;
   const unsigned cap = std::max(1u, 148u * 8u / (unsigned)std::max(1, cm.L));
   dim3 grid(grid_for(per, 256 * 16, cap), cm.L);
@@ -825,7 +835,9 @@ cudaError_t launch_act_bwd(const ChannelMap& cm, const float* gy, const float* y
     case ACT_SIGMOID: act_bwd_kernel<ACT_SIGMOID><<<grid, 256, 0, st>>>(cm, gy, y, slope, g); break;
     default: act_bwd_kernel<ACT_NONE><<<grid, 256, 0, st>>>(cm, gy, y, slope, g); break;
   }
-  return launched();
+  cudaError_t r_ = launched();
+  timing_stop(t0_, st, "hbm act_bwd bytes=" + std::to_string((long long)(12LL * cm.L * cm.R * cm.Cp)));
+  return r_;
 }
 
 cudaError_t launch_bias_finalize(const ChannelMap& cm, const float* partial, float* dbias, long long dbias_ls,
@@ -856,9 +868,12 @@ cudaError_t launch_loss_g(int L, int B, const float* p_fake, int pstride, double
 }
 
 cudaError_t launch_nonfinite_check(int L, long long P, const float* grads, int* flags, cudaStream_t st) {
+  cudaEvent_t t0_ = timing_start(st);
   dim3 grid(grid_for(P / 4, 256, 64), L);
   nonfinite_kernel<<<grid, 256, 0, st>>>(P, grads, flags);
-  return launched();
+  cudaError_t r_ = launched();
+  timing_stop(t0_, st, "hbm nonfinite bytes=" + std::to_string((long long)(4LL * L * P)));
+  return r_;
 }
 
 cudaError_t launch_adam_tick(int L, const int* flags, long long* t, cudaStream_t st) {
@@ -869,16 +884,22 @@ cudaError_t launch_adam_tick(int L, const int* flags, long long* t, cudaStream_t
 cudaError_t launch_adam(int L, long long P, float* params, const float* grads, float* m, float* v,
                         const long long* t, const int* flags, float lr, double b1, double b2, float eps,
                         cudaStream_t st) {
+  cudaEvent_t t0_ = timing_start(st);
   dim3 grid(grid_for(P / 4, 256, 256), L);
   adam_kernel<<<grid, 256, 0, st>>>(P, params, grads, m, v, t, flags, lr, b1, b2, eps);
-  return launched();
+  cudaError_t r_ = launched();
+  timing_stop(t0_, st, "hbm adam bytes=" + std::to_string((long long)(28LL * L * P)));
+  return r_;
 }
 
 cudaError_t launch_gather_real(int L, int B, const int* idx, const float* data, long long data_ls, long long sample,
                                int Cp, int C, float* out, cudaStream_t st) {
+  cudaEvent_t t0_ = timing_start(st);
   dim3 grid(grid_for(sample / 4, 256, 16), B, L);
   gather_real_kernel<<<grid, 256, 0, st>>>(B, idx, data, data_ls, sample, Cp, C, out);
-  return launched();
+  cudaError_t r_ = launched();
+  timing_stop(t0_, st, "hbm gather_real bytes=" + std::to_string((long long)(8LL * L * B * sample)));
+  return r_;
 }
 
 cudaError_t launch_nchw01_to_nhwc(long long N, int C, int H, int W, int Cp, const float* in, float* out,

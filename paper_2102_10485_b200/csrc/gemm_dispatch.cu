@@ -138,10 +138,32 @@ void gemm_timing_enable(bool on) {
   g_timing = on;
 }
 
+cudaEvent_t timing_start(cudaStream_t st) {
+  if (!g_timing) return nullptr;
+  cudaEvent_t e0 = nullptr;
+  cudaEventCreate(&e0);
+  cudaEventRecord(e0, st);
+  return e0;
+}
+
+void timing_stop(cudaEvent_t e0, cudaStream_t st, const std::string& tag) {
+  if (!e0) return;
+  cudaEvent_t e1 = nullptr;
+  cudaEventCreate(&e1);
+  cudaEventRecord(e1, st);
+  std::lock_guard<std::mutex> g(g_mu);
+  g_events.emplace_back(e0, e1);
+  g_tags.emplace_back(tag);
+}
+
+// summed device time of the implicit-GEMM launches (the "hbm ..." tagged
+// elementwise launches of the same report are excluded)
 double gemm_timing_read_ms() {
   std::lock_guard<std::mutex> g(g_mu);
   double total = 0;
-  for (auto& e : g_events) {
+  for (size_t i = 0; i < g_events.size(); ++i) {
+    if (g_tags[i].rfind("hbm", 0) == 0) continue;
+    const auto& e = g_events[i];
     cudaEventSynchronize(e.second);
     float ms = 0;
     cudaEventElapsedTime(&ms, e.first, e.second);

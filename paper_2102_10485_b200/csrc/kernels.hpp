@@ -21,6 +21,9 @@ double gemm_timing_read_ms();
 #include <string>
 namespace pg {
 std::string gemm_timing_report();  // one line per timed GEMM launch: shape tags + ms
+// the same per-launch timing for the HBM-bound kernels: tag "hbm <name> bytes=<algorithmic bytes>"
+cudaEvent_t timing_start(cudaStream_t st);  // nullptr when timing is off
+void timing_stop(cudaEvent_t e0, cudaStream_t st, const std::string& tag);
 
 // measured tcgen05 kind::tf32 dense peak (TFLOP/s), tc_peak.cu
 cudaError_t tc_tf32_peak(int iters, double* tflops);

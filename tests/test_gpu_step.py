@@ -518,3 +518,22 @@ def test_cuda_graph_step_is_bit_identical(monkeypatch):
         for f in (N.F_GEN_PARAMS, N.F_DISC_PARAMS, N.F_GEN_BUFFERS, N.F_DISC_BUFFERS, N.F_GEN_GRADS, N.F_DISC_GRADS,
                   N.F_GEN_ADAM_M, N.F_DISC_ADAM_V, N.F_REPORTS, N.F_LAST_BATCH, N.F_COUNTERS):
             assert eager.get(label, f).tobytes() == graph.get(label, f).tobytes(), (label, f)
+
+
+def test_repeatable_bitwise_at_c4_scale():
+    """Race detector by repetition (the pool's compute-sanitizer is closed):
+    two identical c4 groups of 24 labels x batch 32 -- hundreds of tiles per
+    persistent CTA pair, every mbarrier ring wrapping many times -- must give
+    byte-identical parameters, Adam moments and reports after 2 steps.  A
+    shared-memory or TMEM race would show up as run-to-run differences."""
+    arch = baseline_arch(4)
+    spec = dict(arch=arch, class_ids=list(range(24)), batch=32, per_label=64, base_seed=3, math=1)
+    runs = []
+    for _ in range(2):
+        g = LabelGroup(GroupSpec(**spec))
+        g.generate_dataset(5)
+        assert g.train_steps(2) == 2
+        runs.append(g)
+    for label in (0, 11, 23):
+        for f in (N.F_GEN_PARAMS, N.F_DISC_PARAMS, N.F_GEN_ADAM_V, N.F_DISC_ADAM_M, N.F_GEN_GRADS, N.F_REPORTS):
+            assert runs[0].get(label, f).tobytes() == runs[1].get(label, f).tobytes(), (label, f)
