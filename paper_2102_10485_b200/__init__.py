@@ -5,10 +5,11 @@ kernels + C++ host), bound here through ctypes.  See DESIGN.md.
 """
 from . import _native
 from .archs import CONFIGS, Arch, algorithmic_flops_per_image, baseline_arch
-from .trainer import (AdamConfig, GroupSpec, LabelGroup, StepReport, cosine_label, derive_seed, make_group,
-                      partition_by_label, shard_begin)
+from .trainer import (AdamConfig, GroupSpec, LabelGroup, StepReport, cosine_label, derive_seed, estimate_priors,
+                      make_group, partition_by_label, shard_begin)
 
 __all__ = [
     "_native", "CONFIGS", "Arch", "algorithmic_flops_per_image", "baseline_arch", "AdamConfig", "GroupSpec",
-    "LabelGroup", "StepReport", "cosine_label", "derive_seed", "make_group", "partition_by_label", "shard_begin",
+    "LabelGroup", "StepReport", "cosine_label", "derive_seed", "estimate_priors", "make_group", "partition_by_label",
+    "shard_begin",
 ]

@@ -111,3 +111,17 @@ def _first_linear_macs(spec: str, shape: tuple) -> float:
             oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
             return float(oh * ow * co * ci * k * k)
     return 0.0
+
+
+def with_bn(arch: Arch, eps: float, momentum: float) -> Arch:
+    """the same architecture with explicit BatchNorm epsilon / momentum
+    (RunConfig bn_eps / bn_momentum, layers.hpp:25-29)"""
+    def fix(spec: str) -> str:
+        out = []
+        for item in spec.split(";"):
+            t = item.split()
+            if t and t[0] == "bn":
+                item = f" bn {t[1]} {eps!r} {momentum!r}"
+            out.append(item)
+        return ";".join(out)
+    return Arch(arch.name, fix(arch.gen), fix(arch.disc), arch.image, arch.d_z)

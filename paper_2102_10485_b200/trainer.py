@@ -238,3 +238,19 @@ def partition_by_label(labels, k: int) -> list[np.ndarray]:
         if s.size == 0:
             raise ValueError(f"class {j} has no samples")
     return shards
+
+
+def estimate_priors(shards) -> tuple[np.ndarray, np.ndarray]:
+    """partition.cpp:58-74: per-class counts and counts / total, in class
+    order; shards are (class_id, indices) pairs covering classes 0..k-1."""
+    shards = list(shards)
+    if not shards:
+        raise ValueError("estimate_priors: no shards")
+    counts = np.zeros(len(shards), np.int64)
+    for cid, idx in shards:
+        if cid < 0 or cid >= len(shards):
+            raise ValueError(f"shard class id {cid} out of range")
+        if len(idx) == 0:
+            raise ValueError(f"class {cid} has no samples")
+        counts[cid] = len(idx)
+    return counts, counts / counts.sum()

@@ -537,3 +537,101 @@ def test_repeatable_bitwise_at_c4_scale():
     for label in (0, 11, 23):
         for f in (N.F_GEN_PARAMS, N.F_DISC_PARAMS, N.F_GEN_ADAM_V, N.F_DISC_ADAM_M, N.F_GEN_GRADS, N.F_REPORTS):
             assert runs[0].get(label, f).tobytes() == runs[1].get(label, f).tobytes(), (label, f)
+
+
+def _read_ckpt(path):
+    import json
+    import struct
+    raw = open(path, "rb").read()
+    (hlen,) = struct.unpack("<I", raw[:4])
+    head = json.loads(raw[4:4 + hlen])
+    blobs, at = {}, 4 + hlen
+    for b in head["blobs"]:
+        blobs[b["name"]] = np.frombuffer(raw[at:at + 8 * b["len"]], "<f8").copy()
+        at += 8 * b["len"]
+    return head, blobs
+
+
+def _write_ckpt(path, head, blobs):
+    import json
+    import struct
+    h = json.dumps(head).encode()
+    with open(path, "wb") as f:
+        f.write(struct.pack("<I", len(h)) + h)
+        for b in head["blobs"]:
+            f.write(np.ascontiguousarray(blobs[b["name"]], "<f8").tobytes())
+
+
+CKPT_FIELDS = (("gen_params", 0), ("disc_params", 1), ("gen_buffers", 2), ("disc_buffers", 3), ("opt_g_m", 6),
+               ("opt_g_v", 7), ("opt_d_m", 8), ("opt_d_v", 9))
+
+
+def test_checkpoint_interchange_with_cpu_oracle(oracle, tmp_path):
+    """The checkpoint format is the hand-off between the CPU world and the
+    device (checkpoint.cpp:91-194).  (1) A device-written checkpoint loads
+    into the f64 oracle and both continue the same run: the next step's J_D,
+    D(real), D(fake) and discriminator gradients agree within 1e-4 (forced
+    masks) and the generator gradients within 1e-3 (they follow an Adam step
+    taken from the transferred state).  (2) An oracle state written in the
+    reference format by a CPU-side writer loads into the device bit for bit
+    (as its fp32 cast)."""
+    arch, grp = make_pair(1, 1, 96, 32, 1)
+    orc = oracle.OracleGroup(64, 1, 1, 96, 32, data_seed=3, base_seed=7)
+    assert grp.train_steps(1) == 1
+    orc.step(1)  # same streams: shuffle, z1, z2 consumed in the same order
+    path = tmp_path / "dev.bin"
+    grp.save_checkpoint(0, str(path))
+    head, blobs = _read_ckpt(path)
+    for name, code in CKPT_FIELDS:
+        orc.set(0, code, blobs[name])
+    orc.set(0, OR_COUNTERS, np.array([head["opt_g"]["t"], head["opt_d"]["t"], head["steps"]], float))
+    grp.capture_masks(True)
+    assert grp.train_steps(1) == 1
+    orc.set_masks(0, grp.masks(0))
+    orc.step(1)
+    r, q = grp.reports(0)[-1], orc.get(0, OR["reports"]).reshape(-1, 4)[-1]
+    assert np.all(np.abs(r[[0, 2, 3]] - q[[0, 2, 3]]) <= 1e-4 * np.abs(q[[0, 2, 3]])), (r, q)
+    for code, spec, ish, tol in ((N.F_DISC_GRADS, arch.disc, arch.image, 1e-4),
+                                 (N.F_GEN_GRADS, arch.gen, (arch.d_z,), 1e-3)):
+        g, ref = grp.get(0, code), orc.get(0, code)
+        for name, off, n, feeds_bn in layer_tensors(spec, ish):
+            if not feeds_bn:
+                assert rel_max(g[off:off + n], ref[off:off + n]) < tol, name
+    # (2) oracle -> reference-format file -> device
+    out = {name: orc.get(0, code) for name, code in CKPT_FIELDS}
+    cnt = orc.get(0, OR_COUNTERS)
+    head2 = dict(head)
+    head2["opt_g"] = dict(head["opt_g"], t=int(cnt[0]))
+    head2["opt_d"] = dict(head["opt_d"], t=int(cnt[1]))
+    head2["steps"] = int(cnt[2])
+    p2 = tmp_path / "cpu.bin"
+    _write_ckpt(p2, head2, out)
+    fresh = LabelGroup(GroupSpec(arch=arch, class_ids=[0], batch=32, per_label=96, base_seed=1, math=1))
+    fresh.load_checkpoint(0, str(p2))
+    for name, code in CKPT_FIELDS:
+        assert np.array_equal(fresh.get(0, code), out[name].astype(np.float32).astype(np.float64)), name
+    assert np.array_equal(fresh.get(0, N.F_COUNTERS), cnt)
+
+
+def test_cli_config_and_bench(tmp_path):
+    """train --config (the reference's JSON RunConfig) and the bench command's
+    scaling.csv (run.cpp:516-529 format)."""
+    import json
+    import subprocess
+    import sys
+    cfg = {"epochs": 1, "batch_size": 32, "seed": 3, "out_dir": str(tmp_path / "run"),
+           "dataset": {"kind": "synthetic", "synthetic": {"kind": "cosine-field", "k": 2, "per_class_n": 64,
+                                                          "seed": 4, "image_size": 28}}}
+    (tmp_path / "c.json").write_text(json.dumps(cfg))
+    r = subprocess.run([sys.executable, "-m", "paper_2102_10485_b200", "train", "--config", str(tmp_path / "c.json")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    man = json.loads((tmp_path / "run" / "manifest.json").read_text())
+    assert man["k"] == 2 and man["priors"]["probabilities"] == [0.5, 0.5]
+    assert len((tmp_path / "run" / "losses.csv").read_text().splitlines()) == 1 + 2 * 2
+    r = subprocess.run([sys.executable, "-m", "paper_2102_10485_b200", "bench", "--out", str(tmp_path / "b"), "--k",
+                        "1,3", "--arch", "1", "--per-label", "64", "--batch", "32"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    lines = (tmp_path / "b" / "scaling.csv").read_text().splitlines()
+    assert lines[0] == "k,wall_clock_s,max_worker_s,cores_used,oversubscribed"
+    assert [ln.split(",")[0] for ln in lines[1:]] == ["1", "3"]
