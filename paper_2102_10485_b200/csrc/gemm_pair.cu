@@ -876,10 +876,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
     }
   } else {
     // ===================== MMA issuer (leader CTA only): A from TMEM =====================
-    if (rank == 0 && lane == 0) {
+    // whole warp in the loop (warp-uniform descriptors in uniform registers),
+    // one elected lane issues -- the single-lane divergent form paced these
+    // tiles on instruction issue (as it did the SS kernel, see there)
+    if (rank == 0) {
       constexpr uint32_t idesc = make_idesc(2 * BM, BN, false, B_MN);
       constexpr uint32_t b_lbo = B_MN ? 4096u : 16u, b_sbo = B_MN ? 512u : 1024u, b_step = B_MN ? 1024u : 32u;
       constexpr uint32_t b_lay = B_MN ? UMMA_SW128_BASE32B : UMMA_SW128;
+      const uint64_t bh_desc0 = make_desc(smem_u32(lo_base), b_lbo, b_sbo, b_lay);
+      const uint64_t bl_desc0 = make_desc(smem_u32(lo_base) + LB, b_lbo, b_sbo, b_lay);
       uint32_t it = 0, sc = 0;
       for (int t = cl; t < ntiles; t += ncl) {
         for (int k_seg = 0; k_seg < P.nk; k_seg += P.kseg, ++sc) {
@@ -889,24 +894,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ATM_NT, 1)
           const uint32_t dacc = tmem + buf * BN;
           const int k_end = min(P.nk, k_seg + P.kseg);
           for (int kb = k_seg; kb < k_end; ++kb, ++it) {
-            const int s = it % SH, j = it % ATM_SA;
+            const int j = it % ATM_SA;
             mbar_wait_cluster(ready + j, (it / ATM_SA) & 1);
             tc_fence_after();
             const uint32_t a_t = tmem + ATM_ACOL + j * 64;
-            const uint32_t b_hi = smem_u32(lo_base + j * 2 * LB);
-            const uint32_t b_lo = b_hi + LB;
+            const uint64_t bh0 = bh_desc0 + (uint64_t)((j * 2 * LB) >> 4), bl0 = bl_desc0 + (uint64_t)((j * 2 * LB) >> 4);
+            if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < BKT / 8; ++kk) {
-              const uint64_t bh = make_desc(b_hi + kk * b_step, b_lbo, b_sbo, b_lay);
-              const uint64_t bl = make_desc(b_lo + kk * b_step, b_lbo, b_sbo, b_lay);
-              const uint32_t acc = (kb != k_seg || kk) ? 1u : 0u;
-              mma_tf32_pair_ts(dacc, a_t + 32 + kk * 8, bh, idesc, acc);  // small terms first
-              mma_tf32_pair_ts(dacc, a_t + kk * 8, bl, idesc, 1u);
-              mma_tf32_pair_ts(dacc, a_t + kk * 8, bh, idesc, 1u);
+              for (int kk = 0; kk < BKT / 8; ++kk) {
+                const uint64_t bh = bh0 + (kk * b_step >> 4), bl = bl0 + (kk * b_step >> 4);
+                const uint32_t acc = (kb != k_seg || kk) ? 1u : 0u;
+                mma_tf32_pair_ts(dacc, a_t + 32 + kk * 8, bh, idesc, acc);  // small terms first
+                mma_tf32_pair_ts(dacc, a_t + kk * 8, bl, idesc, 1u);
+                mma_tf32_pair_ts(dacc, a_t + kk * 8, bh, idesc, 1u);
+              }
+              mma_commit_pair(empty_l + j, 3);
+              if (kb + 1 == k_end) mma_commit_pair(seg_full + buf, 3);
             }
-            mma_commit_pair(empty_l + j, 3);
+            __syncwarp();
           }
-          mma_commit_pair(seg_full + buf, 3);
         }
       }
     }
@@ -968,12 +974,16 @@ cudaError_t launch_pair_atm(const CUtensorMap& ta, const CUtensorMap& tb, const 
   return launched();
 }
 
-// A-in-TMEM tiles: correct, but measured no faster than the SS form in the
-// full step (82.6 vs 82.5 ms; the narrow tiles are L2-feed bound), so opt-in
+// A-in-TMEM tiles for the narrow FPROP / DGRAD tiles (default; PG_ATM=0 off).
+// Round 1 measured them no faster: their MMA issuer was a single divergent
+// lane (instruction-issue bound, as the SS kernel had been), and the weight
+// lo pre-split added later was never loaded by this producer (a hang).  With
+// the warp-uniform issuer: conv2 forward 1.13 -> 1.02 ms, conv3 data gradient
+// 1.17 -> 0.98 ms (c4, 125 labels x 32, scripts/gemm_sweep.py).
 bool atm_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PG_ATM");
-    return e && std::atoi(e) != 0;
+    return !(e && e[0] == '0');
   }();
   return on;
 }
@@ -1199,7 +1209,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
     // when the weights are small against the activations (>= 8 output rows per
     // weight row): the split warps then only touch A (conv2
     // forward 1.21 -> 1.11 ms; the wide tiles lose more to the extra pass)
-    if (math == MATH_TF32X3 && bn <= 128 && blo_enabled() && (long long)g.B * g.SH * g.SW >= 8LL * g.CS) {
+    if (math == MATH_TF32X3 && bn <= 128 && blo_enabled() && !atm_enabled() && (long long)g.B * g.SH * g.SW >= 8LL * g.CS) {
       float* wl = blo_buffer((size_t)a.L * K * g.CS, st);
       if (!wl) return cudaErrorMemoryAllocation;
       cudaError_t e = launch_tf32_lo(a.w, a.w_ls, K * g.CS, a.L, wl, st);
@@ -1243,7 +1253,7 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
     const int bbox[4] = {32, 1, BKT, 1};
     ok = ok && make_map(&tb, a.w, 4, bd, bs, bbox, one, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     // b_lo pre-split for the narrow tiles (as FPROP above)
-    if (math == MATH_TF32X3 && bn <= 128 && blo_enabled() && (long long)g.B * g.GH * g.GW >= 8LL * g.CG) {
+    if (math == MATH_TF32X3 && bn <= 128 && blo_enabled() && !atm_enabled() && (long long)g.B * g.GH * g.GW >= 8LL * g.CG) {
       const long long nw = (long long)g.CS * kk * g.CG;
       float* wl = blo_buffer((size_t)a.L * nw, st);
       if (!wl) return cudaErrorMemoryAllocation;
