@@ -251,7 +251,9 @@ def main():
         dist.barrier()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    imgs = world * Lg * args.batch * ran
+    # exact images in the timed steps: an epoch ends with a partial tail batch
+    # when per_label is not a multiple of the batch (run_worker, partition.cpp:92-96)
+    imgs = world * Lg * images_in_steps(args.warmup, ran, args.per_label, args.batch)
     value = imgs / (max_ms / 1000.0)
 
     # per-kernel timing pass (separate from the headline): implicit-GEMM share,
@@ -268,7 +270,7 @@ def main():
     lib.pg_kernel_timing(0)
     timing_lines = rep_buf.value.decode().splitlines()
     flops_img = algorithmic_flops_per_image(arch)
-    step_flops = Lg * args.batch * flops_img
+    step_flops = Lg * images_in_steps(args.warmup + ran, 1, args.per_label, args.batch) * flops_img
     peaks = measured_peaks()
     achieved = step_flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
     # denominator: this GPU's tcgen05 kind::tf32 dense rate, measured live by
@@ -362,6 +364,16 @@ def main():
     grp.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def images_in_steps(first: int, n: int, per_label: int, batch: int) -> int:
+    """images one label consumes in steps [first, first + n) of the worker protocol"""
+    spe = -(-per_label // batch)
+    total = 0
+    for s in range(first, first + n):
+        pos = s % spe
+        total += min(batch, per_label - pos * batch)
+    return total
 
 
 def kernel_classes(lines, tf32_peak, hbm_gbs):

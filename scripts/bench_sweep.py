@@ -16,9 +16,13 @@ RUNS = [
     ("c4 sweep B=32", ["--cfg", "4", "--labels-per-gpu", "125", "--batch", "32"]),
     ("c4 sweep B=64", ["--cfg", "4", "--labels-per-gpu", "125", "--batch", "64"]),
     ("c4 sweep B=128", ["--cfg", "4", "--labels-per-gpu", "125", "--batch", "128"]),
-    ("c1 (10 labels, B=64)", ["--cfg", "1", "--labels-per-gpu", "10", "--batch", "64", "--per-label", "6000"]),
-    ("c2 (10 labels, B=64)", ["--cfg", "2", "--labels-per-gpu", "10", "--batch", "64", "--per-label", "5000"]),
-    ("c3 (13 labels/GPU, B=32)", ["--cfg", "3", "--labels-per-gpu", "13", "--batch", "32", "--per-label", "500"]),
+    # the small configurations are launch-latency scale: 300 timed steps so the clock sampler sees the run
+    ("c1 (10 labels, B=64)", ["--cfg", "1", "--labels-per-gpu", "10", "--batch", "64", "--per-label", "6000",
+                             "--steps", "300"]),
+    ("c2 (10 labels, B=64)", ["--cfg", "2", "--labels-per-gpu", "10", "--batch", "64", "--per-label", "5000",
+                             "--steps", "300"]),
+    ("c3 (13 labels/GPU, B=32)", ["--cfg", "3", "--labels-per-gpu", "13", "--batch", "32", "--per-label", "500",
+                                 "--steps", "300"]),
 ]
 
 p = argparse.ArgumentParser()
@@ -30,8 +34,8 @@ with open(args.out, "a") as f:
     for name, extra in RUNS:
         if args.only and args.only not in name:
             continue
-        cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--steps", str(args.steps), "--warmup", "3",
-               "--no-cpu-baseline", *extra]
+        steps = [] if "--steps" in extra else ["--steps", str(args.steps)]
+        cmd = [sys.executable, os.path.join(ROOT, "bench.py"), *steps, "--warmup", "3", "--no-cpu-baseline", *extra]
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
         line = next((ln for ln in reversed(r.stdout.splitlines()) if ln.startswith("{")), None)
         rec = {"run": name, "rc": r.returncode}
