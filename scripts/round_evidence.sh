@@ -10,7 +10,7 @@ SHORT="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --ga
 timeout 600 $SHORT > gpurun_out/bench_short.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 1500 --csv --log-file gpurun_out/launches.csv $SHORT > gpurun_out/ncu_launches.log 2>&1
 echo "launches rc=$?" >> gpurun_out/ncu_launches.log
-for spec in "conv_wgrad 4" "conv_fwd 3"; do
+for spec in "conv_dgrad 2" "conv_fwd 2" "conv_wgrad 2"; do
   set -- $spec
   bash scripts/ncu_text.sh top_$1_$2 gemm_pair python scripts/gemm_bench.py --op $1 --layer $2 --iters 1
 done
