@@ -13,9 +13,6 @@
 //   scatter is a deterministic gather (each output sums its <= (k/s)^2 taps in
 //   a fixed order).
 // The im2col / P buffers live in the grow-only GEMM scratch (stream-ordered).
-#include <algorithm>
-#include <cstdlib>
-
 #include "kernels.hpp"
 
 namespace pg {
@@ -178,45 +175,28 @@ cudaError_t launch_gemm_lowered(const GemmArgs& a, int math, cudaStream_t st) {
     p.stat_slope = a.stat_slope;
     return launch_gemm_pair(p, math, st);
   }
-  // DGRAD: columns P = small . Wt, then the col2im gather -- in chunks of
-  // labels whose P (8.4 MB per c4 label) stays resident in L2 between the GEMM
-  // that writes it and the gather that reads it (PG_LOWERED_CHUNK labels;
-  // 0 = all labels at once)
+  // DGRAD: columns P = small . Wt, then the col2im gather
   const long long wt_ls = (long long)kk * 4 * g.CS;
   const long long p_ls = pix * kk * 4;
-  static const int chunk_env = [] {
-    const char* e = std::getenv("PG_LOWERED_CHUNK");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int chunk = a.stat_mode == STAT_NONE && chunk_env > 0 ? std::min(chunk_env, a.L) : a.L;
   const size_t wt_floats = (size_t)(wt_ls * a.L + 63) / 64 * 64;
-  float* scratch = gemm_scratch(wt_floats + (size_t)(p_ls * chunk), st);
+  float* scratch = gemm_scratch(wt_floats + (size_t)(p_ls * a.L), st);
   if (!scratch) return cudaErrorMemoryAllocation;
   float* wt = scratch;
   float* P = scratch + wt_floats;
   wt_transpose4_kernel<<<blocks_for(wt_ls * a.L, 256), 256, 0, st>>>(g, a.L, a.w, a.w_ls, wt);
   cudaError_t e = launched();
   if (e != cudaSuccess) return e;
-  for (int l0 = 0; l0 < a.L; l0 += chunk) {
-    GemmArgs c = a;
-    c.L = std::min(chunk, a.L - l0);
-    c.small = a.small + l0 * a.small_ls;
-    c.out = a.out + l0 * a.out_ls;
-    if (a.bias) c.bias = a.bias + l0 * a.bias_ls;
-    GemmArgs p = fprop_1x1(c, g.B, g.SH, g.SW, g.CS, kk * 4);
-    p.big = c.small;
-    p.big_ls = a.small_ls;
-    p.w = wt + l0 * wt_ls;
-    p.w_ls = wt_ls;
-    p.out = P;
-    p.out_ls = p_ls;
-    e = launch_gemm_pair(p, math, st);
-    if (e != cudaSuccess) return e;
-    col2im4_kernel<<<blocks_for((long long)g.B * g.GH * g.GW * c.L, 256), 256, 0, st>>>(c, P);
-    e = launched();
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  GemmArgs p = fprop_1x1(a, g.B, g.SH, g.SW, g.CS, kk * 4);
+  p.big = a.small;
+  p.big_ls = a.small_ls;
+  p.w = wt;
+  p.w_ls = wt_ls;
+  p.out = P;
+  p.out_ls = p_ls;
+  e = launch_gemm_pair(p, math, st);
+  if (e != cudaSuccess) return e;
+  col2im4_kernel<<<blocks_for((long long)g.B * g.GH * g.GW * a.L, 256), 256, 0, st>>>(a, P);
+  return launched();
 }
 
 }  // namespace pg
