@@ -55,6 +55,16 @@ GanGroup::GanGroup(const GroupConfig& cfg) : cfg_(cfg), L_(static_cast<int>(cfg.
   check_cuda(cudaStreamCreateWithFlags(&cst_, cudaStreamNonBlocking), "copy stream");
   check_cuda(cudaEventCreateWithFlags(&real_ready_, cudaEventDisableTiming), "event");
   tg_ = G_->make_trace(true);
+  {
+    const char* e = std::getenv("PG_OVERLAP");
+    overlap_ = !(e && e[0] == '0');
+  }
+  if (overlap_) {
+    tg2_ = G_->make_trace(true);
+    check_cuda(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream 2");
+    for (cudaEvent_t* ev : {&ev_fork_, &ev_g1_, &ev_g2_})
+      check_cuda(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
+  }
   tdr_ = D_->make_trace(true);
   tdf_ = D_->make_trace(true);
   zcp_ = pad4(cfg_.d_z);
@@ -133,6 +143,13 @@ GanGroup::~GanGroup() {
     cudaStreamDestroy(cst_);
   }
   if (real_ready_) cudaEventDestroy(real_ready_);
+  for (cudaEvent_t ev : {ev_fork_, ev_g1_, ev_g2_})
+    if (ev) cudaEventDestroy(ev);
+  if (st2_) {
+    cudaStreamSynchronize(st2_);
+    release_stream_scratch(st2_);
+    cudaStreamDestroy(st2_);
+  }
   for (int par = 0; par < 2; ++par) {
     cudaFree(d_idx_[par]);
     cudaFreeHost(h_idx_[par]);
@@ -230,6 +247,15 @@ void GanGroup::prep_host(int par, int B, bool with_idx) {
 }
 
 // The adversarial step (gan.cpp:136-176) for all labels, on st_.
+static long long act_mask_bytes(const DevNet& net, int B) {
+  long long n = 0;
+  for (int i = 0; i < net.blocks(); ++i) {
+    const Block& b = net.block(i);
+    if (b.act == ACT_RELU || b.act == ACT_LRELU) n += static_cast<long long>(B) * b.out.C * b.out.H * b.out.W;
+  }
+  return n;
+}
+
 void GanGroup::enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t real_ready) {
   enqueue_step_kernels(B, real_nhwc, par, real_ready, d_rep_ + (steps_ % rep_cap_) * L_ * 4);
   steps_ += 1;
@@ -238,21 +264,44 @@ void GanGroup::enqueue_step(int B, const float* real_nhwc, int par, cudaEvent_t 
 }
 
 // The kernels of one step (gan.cpp:136-176), enqueued on st_; reports to rep.
+// With overlap on (PG_OVERLAP, default), both generator forwards -- they depend
+// only on G's parameters, which the discriminator half of the step does not
+// touch -- run on a second stream (z2 into its own trace): G(z1) beside
+// D(real), G(z2) beside the whole discriminator update; st_ joins each before
+// the pass that reads it.  The kernels and their order per network are
+// unchanged, so results are bit-identical to the serial order.
 void GanGroup::enqueue_step_kernels(int B, const float* real_nhwc, int par, cudaEvent_t real_ready, double* rep) {
   const int pstride = static_cast<int>(D_->out_map().Cp);
   const int nbg = G_->blocks(), nbd = D_->blocks();
-  long long moff = 0;  // mask capture (parity instrumentation), in the order the passes run
+  // mask capture (parity instrumentation): segment offsets in the order G z1, D real, D fake, G z2, D fake
+  const long long gsz = capture_ ? act_mask_bytes(*G_, B) : 0, dsz = capture_ ? act_mask_bytes(*D_, B) : 0;
+  const bool ov = overlap_;
+  cudaStream_t gs = ov ? st2_ : st_;
+  Trace& tg2 = ov ? tg2_ : tg_;
+  if (ov) {
+    check_cuda(cudaEventRecord(ev_fork_, st_), "fork");
+    check_cuda(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork wait");
+  }
   // discriminator update on (real, fresh fake); the generator trace is dropped
   tg_.act[0] = dz_[par][0].p;
-  G_->forward(tg_, B, true, true, st_);
-  if (capture_) moff = capture_pass(*G_, tg_, B, moff);
+  G_->forward(tg_, B, true, true, gs);
+  if (capture_) capture_pass(*G_, tg_, B, 0, gs);
+  if (ov) {
+    check_cuda(cudaEventRecord(ev_g1_, st2_), "g1");
+    // the generator step's forward (z2) right behind it, into its own trace
+    tg2.act[0] = dz_[par][1].p;
+    G_->forward(tg2, B, true, true, st2_);
+    if (capture_) capture_pass(*G_, tg2, B, gsz + 2 * dsz, st2_);
+    check_cuda(cudaEventRecord(ev_g2_, st2_), "g2");
+  }
   tdr_.act[0] = const_cast<float*>(real_nhwc);
   if (real_ready) check_cuda(cudaStreamWaitEvent(st_, real_ready, 0), "wait real batch");
   D_->forward(tdr_, B, true, true, st_);
-  if (capture_) moff = capture_pass(*D_, tdr_, B, moff);
+  if (capture_) capture_pass(*D_, tdr_, B, gsz, st_);
+  if (ov) check_cuda(cudaStreamWaitEvent(st_, ev_g1_, 0), "join g1");
   tdf_.act[0] = tg_.act[static_cast<size_t>(nbg)];
   D_->forward(tdf_, B, true, true, st_);
-  if (capture_) moff = capture_pass(*D_, tdf_, B, moff);
+  if (capture_) capture_pass(*D_, tdf_, B, gsz + dsz, st_);
   check_cuda(launch_loss_d(L_, B, tdr_.act[static_cast<size_t>(nbd)], tdf_.act[static_cast<size_t>(nbd)], pstride,
                            cfg_.clamp, gp_real_.p, gp_fake_.p, rep, st_),
              "loss_d");
@@ -265,19 +314,23 @@ void GanGroup::enqueue_step_kernels(int B, const float* real_nhwc, int par, cuda
                          static_cast<float>(cfg_.eps), st_),
              "adam D");
   // generator update through the updated discriminator (its grads discarded)
-  tg_.act[0] = dz_[par][1].p;
-  G_->forward(tg_, B, true, true, st_);
-  if (capture_) moff = capture_pass(*G_, tg_, B, moff);
-  tdf_.act[0] = tg_.act[static_cast<size_t>(nbg)];
+  if (ov) {
+    check_cuda(cudaStreamWaitEvent(st_, ev_g2_, 0), "join g2");
+  } else {
+    tg_.act[0] = dz_[par][1].p;
+    G_->forward(tg_, B, true, true, st_);
+    if (capture_) capture_pass(*G_, tg_, B, gsz + 2 * dsz, st_);
+  }
+  tdf_.act[0] = tg2.act[static_cast<size_t>(nbg)];
   D_->forward(tdf_, B, true, true, st_);
   if (capture_) {
-    moff = capture_pass(*D_, tdf_, B, moff);
-    mask_len_ = moff;
+    capture_pass(*D_, tdf_, B, 2 * gsz + 2 * dsz, st_);
+    mask_len_ = 2 * gsz + 3 * dsz;
   }
   check_cuda(launch_loss_g(L_, B, tdf_.act[static_cast<size_t>(nbd)], pstride, cfg_.clamp, gp_fake_.p, rep, st_),
              "loss_g");
   D_->backward(tdf_, B, gp_fake_.p, false, false, gimg_.p, st_);
-  G_->backward(tg_, B, gimg_.p, true, false, nullptr, st_);
+  G_->backward(tg2, B, gimg_.p, true, false, nullptr, st_);
   check_cuda(launch_nonfinite_check(L_, G_->P(), G_->grads.p, d_flags_, st_), "nonfinite G");
   check_cuda(launch_adam_tick(L_, d_flags_, d_t_g_, st_), "tick G");
   check_cuda(launch_adam(L_, G_->P(), G_->params.p, G_->grads.p, G_->adam_m.p, G_->adam_v.p, d_t_g_, d_flags_,
@@ -327,15 +380,6 @@ bool GanGroup::launch_step_graph(int B, int par) {
   return true;
 }
 
-static long long act_mask_bytes(const DevNet& net, int B) {
-  long long n = 0;
-  for (int i = 0; i < net.blocks(); ++i) {
-    const Block& b = net.block(i);
-    if (b.act == ACT_RELU || b.act == ACT_LRELU) n += static_cast<long long>(B) * b.out.C * b.out.H * b.out.W;
-  }
-  return n;
-}
-
 void GanGroup::capture_masks(bool on) {
   sync();
   capture_ = on;
@@ -348,14 +392,14 @@ void GanGroup::capture_masks(bool on) {
   }
 }
 
-long long GanGroup::capture_pass(DevNet& net, Trace& t, int B, long long off) {
+long long GanGroup::capture_pass(DevNet& net, Trace& t, int B, long long off, cudaStream_t st) {
   for (int i = 0; i < net.blocks(); ++i) {
     const Block& b = net.block(i);
     if (b.act != ACT_RELU && b.act != ACT_LRELU) continue;
     check_cuda(launch_mask_capture(L_, B, static_cast<int>(b.out.H), static_cast<int>(b.out.W),
                                    static_cast<int>(b.out.C), static_cast<int>(b.out.Cp),
                                    static_cast<long long>(B) * b.out.numel(), t.act[static_cast<size_t>(i) + 1], b.act,
-                                   d_mask_ + off, mask_stride_, st_),
+                                   d_mask_ + off, mask_stride_, st),
                "mask capture");
     off += static_cast<long long>(B) * b.out.C * b.out.H * b.out.W;
   }

@@ -134,7 +134,12 @@ class GanGroup {
   unsigned char* d_mask_ = nullptr;
   long long mask_stride_ = 0;  // bytes per label
   long long mask_len_ = 0;     // bytes per label used by the last step
-  long long capture_pass(DevNet& net, Trace& t, int B, long long off);
+  long long capture_pass(DevNet& net, Trace& t, int B, long long off, cudaStream_t st);
+  // generator forwards on a second stream (see enqueue_step_kernels)
+  bool overlap_ = true;
+  cudaStream_t st2_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_g1_ = nullptr, ev_g2_ = nullptr;
+  Trace tg2_;
 
   uint64_t worker_seed(int l) const;
   void generate_rounds(long n, const std::function<void(int, int, long, float*)>& fill_z, float* out);
