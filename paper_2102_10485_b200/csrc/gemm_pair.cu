@@ -53,6 +53,15 @@ constexpr int BKT = 32;   // fp32 of K per k-block (one 128-byte row)
 #ifndef PG_NSPLIT_WG
 #define PG_NSPLIT_WG 2
 #endif
+#ifndef PG_WIDE_REGS
+#define PG_WIDE_REGS 1  // setmaxnreg hand-off to the drain warps of the BN = 256 tiles
+#endif
+#ifndef PG_REGS_LO
+#define PG_REGS_LO 56
+#endif
+#ifndef PG_REGS_HI
+#define PG_REGS_HI 224
+#endif
 __host__ __device__ constexpr int nsplit(int kind, int bn, int mode) {
   return mode != MATH_TF32X3 || bn > 128 ? 2 : kind == GEMM_WGRAD ? PG_NSPLIT_WG : PG_NSPLIT_NARROW;
 }
@@ -565,9 +574,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
   // it overlaps the previous kernel's tail; no global data is read before this
   grid_dep_wait();
   grid_dep_launch();
+  // wide tiles: the drain holds 128 fp32 partial sums per thread; at the
+  // 168-register cap of 384 threads it spilled (40-104 B/thread).  Warps 0-3
+  // (TMA, split, MMA) are one warpgroup and hand registers to the drain; each
+  // role calls it inside its own branch so ptxas sees the limit of the region.
+  constexpr bool WREGS = BN > 128 && PG_WIDE_REGS;
+  static_assert(!WREGS || W_DR == 4, "producer roles must fill warpgroup 0");
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
+    if constexpr (WREGS) regs_dec<PG_REGS_LO>();
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
@@ -618,6 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
     }
   } else if (warp <= NSPLIT) {
     // ===================== lo split / landed forward (both CTAs) =====================
+    if constexpr (WREGS) regs_dec<PG_REGS_LO>();
     const int st = tid - 32;
     const uint32_t ready_leader = mapa_shared(smem_u32(ready), 0);
     uint32_t it = 0;
@@ -647,6 +664,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
     }
   } else if (warp == W_MMA) {
     // ===================== MMA issuer (leader CTA only) =====================
+    if constexpr (WREGS) regs_dec<PG_REGS_LO>();
     // The whole warp runs the loop (warp-uniform values stay in uniform
     // registers); one elected lane issues the MMAs and the commits.  With a
     // divergent single-lane loop every MMA paid ~12 instructions of R2UR /
@@ -705,6 +723,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
     }
     __syncwarp();
   } else {
+    if constexpr (WREGS) regs_inc<PG_REGS_HI>();
     pair_drain_role<KIND, BN, STATS, NB>(P, tmem, seg_full, seg_empty, warp - W_DR, warp, lane, rank, cl, ncl,
                                          ntiles);
   }

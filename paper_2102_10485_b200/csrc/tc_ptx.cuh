@@ -158,6 +158,13 @@ PG_DEV void tbox(uint32_t dst, const void* tmap, uint64_t* bar, int c0, int c1, 
 PG_DEV void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 PG_DEV void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// move registers between warpgroups of one CTA (every warp of the warpgroup
+// executes it; the increase waits until the decrease has freed enough)
+template <uint32_t N>
+PG_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+template <uint32_t N>
+PG_DEV void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+
 // one lane of the (fully active) warp: the lowest; the same lane every call
 PG_DEV bool elect_one() {
   uint32_t pred = 0;
