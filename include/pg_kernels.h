@@ -12,7 +12,7 @@
  *     step in lockstep;
  *   - device pointers, fp32, NHWC maps with channels padded to a multiple of 4
  *     (pad channels hold zeros), caller-owned memory, stream-ordered, no
- *     allocation inside; weights in the device layouts documented per call;
+ *     allocation inside once a workspace is attached (pg_set_workspace); weights in the device layouts documented per call;
  *   - deterministic: fixed-order reductions, no float atomics.
  * Status: PG_OK or a negative code; pg_last_error() describes the failure.
  */
@@ -89,6 +89,28 @@ int pg_dense_bwd_data(int L, int B, int in, int out, const float* gy, const floa
                       int math, void* stream);
 int pg_dense_bwd_filter(int L, int B, int in, int out, const float* x, const float* gy, float* gw, long long gw_ls,
                         int accumulate, int math, void* stream);
+
+/* ---- Workspace (the C-ABI never allocates) ----
+ * Some GEMM shapes need device scratch inside one call: the split-K partials of
+ * the 4-channel weight gradient, the column matrix of the lowered
+ * 4-channel ConvTranspose2d forward / Conv2d data gradient, and (PG_ATM=0
+ * builds of the narrow tiles) the pre-split tf32 lo part of the weights.
+ * pg_workspace_size returns the bytes operator `op` with descriptor d (Dense:
+ * B, Cin = in, Cout = out, the rest ignored) over L labels in `math` takes
+ * (0 for most shapes; (size_t)-1 on an invalid descriptor, see pg_last_error).
+ * pg_set_workspace attaches a caller-owned device buffer (256-byte aligned) to
+ * a stream on the current device: every later call on that stream carves its
+ * scratch from it and never allocates; a call whose need exceeds it fails with
+ * PG_EINVAL.  NULL detaches (the library then keeps its own grow-only buffer per
+ * stream, as it does when no workspace was ever attached).  The buffer must
+ * stay valid until the stream's last call using it has completed. */
+enum {
+  PG_OP_CONV2D_FWD = 0, PG_OP_CONV2D_BWD_DATA = 1, PG_OP_CONV2D_BWD_FILTER = 2,
+  PG_OP_CONVT2D_FWD = 3, PG_OP_CONVT2D_BWD_DATA = 4, PG_OP_CONVT2D_BWD_FILTER = 5,
+  PG_OP_DENSE_FWD = 6, PG_OP_DENSE_BWD_DATA = 7, PG_OP_DENSE_BWD_FILTER = 8
+};
+size_t pg_workspace_size(int op, const pg_conv_desc* d, int L, int math);
+int pg_set_workspace(void* stream, void* workspace, size_t bytes);
 
 /* ---- BatchNorm over NHWC maps (replaces bn_fwd / bn_bwd, network.cpp:163-271) ----
  * x, y: [L][R][Cp] with R = B*H*W rows per label; gamma_beta [L][2C] (stride gb_ls);

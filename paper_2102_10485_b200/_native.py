@@ -16,6 +16,8 @@ LIB_PATH = Path(os.environ.get("PG_LIB", "")) if os.environ.get("PG_LIB") else \
 PG_OK, PG_EINVAL, PG_ECUDA, PG_ENONFINITE, PG_EUNSUPPORTED = 0, -1, -2, -3, -4
 MATH_FP32_SIMT, MATH_TF32X3, MATH_TF32 = 0, 1, 2
 ACT_NONE, ACT_RELU, ACT_LRELU, ACT_TANH, ACT_SIGMOID = 0, 1, 2, 3, 4
+(PG_OP_CONV2D_FWD, PG_OP_CONV2D_BWD_DATA, PG_OP_CONV2D_BWD_FILTER, PG_OP_CONVT2D_FWD, PG_OP_CONVT2D_BWD_DATA,
+ PG_OP_CONVT2D_BWD_FILTER, PG_OP_DENSE_FWD, PG_OP_DENSE_BWD_DATA, PG_OP_DENSE_BWD_FILTER) = range(9)
 
 (F_GEN_PARAMS, F_DISC_PARAMS, F_GEN_BUFFERS, F_DISC_BUFFERS, F_GEN_GRADS, F_DISC_GRADS, F_GEN_ADAM_M,
  F_GEN_ADAM_V, F_DISC_ADAM_M, F_DISC_ADAM_V, F_REPORTS, F_LAST_BATCH, F_COUNTERS) = range(13)
@@ -66,6 +68,8 @@ _SIGNATURES = {
     "pg_dense_bwd_data": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _LL, _P, C.c_int, _P]),
     "pg_dense_bwd_filter": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _LL, C.c_int, C.c_int, _P]),
     "pg_bn_workspace_floats": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
+    "pg_workspace_size": (C.c_size_t, [C.c_int, C.POINTER(ConvDesc), C.c_int, C.c_int]),
+    "pg_set_workspace": (C.c_int, [_P, _P, C.c_size_t]),
     "pg_bn_fwd": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _LL, _P, _LL, C.c_float, C.c_float, C.c_int,
                             C.c_int, C.c_float, _P, _P, _P, _P, _P]),
     "pg_bn_bwd": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P, _P, _LL, C.c_int, C.c_float, _P, _P,

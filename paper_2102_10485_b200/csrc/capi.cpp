@@ -4,6 +4,7 @@
 
 #include "../../include/pg_trainer.h"
 #include "capi_util.hpp"
+#include "device_cache.hpp"
 #include "gan.hpp"
 
 namespace pg {
@@ -119,193 +120,191 @@ long pg_kernel_timing_report(char* out, long cap) {
   return static_cast<long>(r.size());
 }
 
+// ---------------- GEMM-shaped operators ----------------
+// One argument builder per operator: the operator entry points and
+// pg_workspace_size share it, so the size query sees the engine the call takes.
+}  // extern "C"
+namespace {
+struct OpPtrs {
+  const float* in = nullptr;   // x (forward), gy (data grad), x (filter grad)
+  const float* in2 = nullptr;  // gy of the filter grads
+  const float* w = nullptr;
+  long long w_ls = 0;
+  const float* bias = nullptr;
+  long long bias_ls = 0;
+  int act = PG_ACT_NONE;
+  float slope = 0.f;
+  float* out = nullptr;
+  long long out_ls = 0;  // filter grads: gw_ls
+  int accumulate = 0;
+};
+
+pg::GemmArgs op_args(int op, const pg_conv_desc* d, int L, const OpPtrs& p) {
+  const bool dense = op >= PG_OP_DENSE_FWD;
+  const bool transposed = op >= PG_OP_CONVT2D_FWD && !dense;
+  if (op < PG_OP_CONV2D_FWD || op > PG_OP_DENSE_BWD_FILTER) throw std::invalid_argument("unknown operator id");
+  if (!d) throw std::invalid_argument("invalid convolution descriptor");
+  if (L < 0) throw std::invalid_argument("L must be >= 0");
+  if (!dense) check_desc(d, transposed);
+  pg::GemmArgs a{};
+  a.g = dense ? dense_geo(d->B, d->Cin, d->Cout) : transposed ? convT_geo(d) : conv_geo(d);
+  a.L = L;
+  a.w = p.w;
+  a.w_ls = p.w_ls;
+  const int role = (op - PG_OP_CONV2D_FWD) % 3;  // 0 forward, 1 data grad, 2 filter grad
+  // forward of Conv2d / Dense = FPROP (big -> small); ConvT forward = DGRAD (small -> big)
+  const bool fwd_is_fprop = !transposed;
+  if (role == 0) {
+    a.kind = fwd_is_fprop ? pg::GEMM_FPROP : pg::GEMM_DGRAD;
+    if (fwd_is_fprop) {
+      a.big = p.in;
+      a.big_ls = big_ls(a.g);
+      a.out_ls = small_ls(a.g);
+      a.c_valid = d->Cout;
+      a.c_pad = a.g.CS;
+    } else {
+      a.small = p.in;
+      a.small_ls = small_ls(a.g);
+      a.out_ls = big_ls(a.g);
+      a.c_valid = d->Cout;
+      a.c_pad = a.g.CG;
+    }
+    a.out = p.out;
+    a.bias = p.bias;
+    a.bias_ls = p.bias_ls;
+    a.act = p.act;
+    a.slope = p.slope;
+  } else if (role == 1) {
+    a.kind = fwd_is_fprop ? pg::GEMM_DGRAD : pg::GEMM_FPROP;
+    if (fwd_is_fprop) {
+      a.small = p.in;
+      a.small_ls = small_ls(a.g);
+      a.out_ls = big_ls(a.g);
+      a.c_valid = d->Cin;
+      a.c_pad = a.g.CG;
+    } else {
+      a.big = p.in;
+      a.big_ls = big_ls(a.g);
+      a.out_ls = small_ls(a.g);
+      a.c_valid = d->Cin;
+      a.c_pad = a.g.CS;
+    }
+    a.out = p.out;
+  } else {
+    a.kind = pg::GEMM_WGRAD;
+    // Conv2d / Dense: x is the big map, gy the small one; ConvT: the reverse
+    a.small = fwd_is_fprop ? p.in2 : p.in;
+    a.big = fwd_is_fprop ? p.in : p.in2;
+    a.small_ls = small_ls(a.g);
+    a.big_ls = big_ls(a.g);
+    a.out = p.out;
+    a.out_ls = p.out_ls;
+    a.accumulate = p.accumulate;
+  }
+  return a;
+}
+
+int run_op(int op, const pg_conv_desc* d, int L, const OpPtrs& p, int math, void* stream, const char* what) {
+  return guard([&] {
+    const pg::GemmArgs a = op_args(op, d, L, p);
+    cuda_ok(pg::launch_gemm(a, math, S(stream)), what);
+  });
+}
+
+pg_conv_desc dense_desc(int B, int in, int out) { return pg_conv_desc{B, in, 1, 1, out, 1, 1, 1, 1, 0}; }
+}  // namespace
+extern "C" {
+
 // ---------------- Conv2d ----------------
 int pg_conv2d_fwd(const pg_conv_desc* d, int L, const float* x, const float* w, long long w_ls, const float* bias,
                   long long bias_ls, int act, float slope, float* y, int math, void* stream) {
-  return guard([&] {
-    check_desc(d, false);
-    pg::GemmArgs a{};
-    a.kind = pg::GEMM_FPROP;
-    a.g = conv_geo(d);
-    a.L = L;
-    a.big = x;
-    a.big_ls = big_ls(a.g);
-    a.w = w;
-    a.w_ls = w_ls;
-    a.out = y;
-    a.out_ls = small_ls(a.g);
-    a.bias = bias;
-    a.bias_ls = bias_ls;
-    a.act = act;
-    a.slope = slope;
-    a.c_valid = d->Cout;
-    a.c_pad = a.g.CS;
-    cuda_ok(pg::launch_gemm(a, math, S(stream)), "conv2d_fwd");
-  });
+  OpPtrs p;
+  p.in = x, p.w = w, p.w_ls = w_ls, p.bias = bias, p.bias_ls = bias_ls, p.act = act, p.slope = slope, p.out = y;
+  return run_op(PG_OP_CONV2D_FWD, d, L, p, math, stream, "conv2d_fwd");
 }
 
 int pg_conv2d_bwd_data(const pg_conv_desc* d, int L, const float* gy, const float* w, long long w_ls, float* gx,
                        int math, void* stream) {
-  return guard([&] {
-    check_desc(d, false);
-    pg::GemmArgs a{};
-    a.kind = pg::GEMM_DGRAD;
-    a.g = conv_geo(d);
-    a.L = L;
-    a.small = gy;
-    a.small_ls = small_ls(a.g);
-    a.w = w;
-    a.w_ls = w_ls;
-    a.out = gx;
-    a.out_ls = big_ls(a.g);
-    a.c_valid = d->Cin;
-    a.c_pad = a.g.CG;
-    cuda_ok(pg::launch_gemm(a, math, S(stream)), "conv2d_bwd_data");
-  });
+  OpPtrs p;
+  p.in = gy, p.w = w, p.w_ls = w_ls, p.out = gx;
+  return run_op(PG_OP_CONV2D_BWD_DATA, d, L, p, math, stream, "conv2d_bwd_data");
 }
 
 int pg_conv2d_bwd_filter(const pg_conv_desc* d, int L, const float* x, const float* gy, float* gw, long long gw_ls,
                          int accumulate, int math, void* stream) {
-  return guard([&] {
-    check_desc(d, false);
-    pg::GemmArgs a{};
-    a.kind = pg::GEMM_WGRAD;
-    a.g = conv_geo(d);
-    a.L = L;
-    a.small = gy;
-    a.small_ls = small_ls(a.g);
-    a.big = x;
-    a.big_ls = big_ls(a.g);
-    a.out = gw;
-    a.out_ls = gw_ls;
-    a.accumulate = accumulate;
-    cuda_ok(pg::launch_gemm(a, math, S(stream)), "conv2d_bwd_filter");
-  });
+  OpPtrs p;
+  p.in = x, p.in2 = gy, p.out = gw, p.out_ls = gw_ls, p.accumulate = accumulate;
+  return run_op(PG_OP_CONV2D_BWD_FILTER, d, L, p, math, stream, "conv2d_bwd_filter");
 }
 
 // ---------------- ConvTranspose2d ----------------
 int pg_convT2d_fwd(const pg_conv_desc* d, int L, const float* x, const float* w, long long w_ls, const float* bias,
                    long long bias_ls, int act, float slope, float* y, int math, void* stream) {
-  return guard([&] {
-    check_desc(d, true);
-    pg::GemmArgs a{};
-    a.kind = pg::GEMM_DGRAD;
-    a.g = convT_geo(d);
-    a.L = L;
-    a.small = x;
-    a.small_ls = small_ls(a.g);
-    a.w = w;
-    a.w_ls = w_ls;
-    a.out = y;
-    a.out_ls = big_ls(a.g);
-    a.bias = bias;
-    a.bias_ls = bias_ls;
-    a.act = act;
-    a.slope = slope;
-    a.c_valid = d->Cout;
-    a.c_pad = a.g.CG;
-    cuda_ok(pg::launch_gemm(a, math, S(stream)), "convT2d_fwd");
-  });
+  OpPtrs p;
+  p.in = x, p.w = w, p.w_ls = w_ls, p.bias = bias, p.bias_ls = bias_ls, p.act = act, p.slope = slope, p.out = y;
+  return run_op(PG_OP_CONVT2D_FWD, d, L, p, math, stream, "convT2d_fwd");
 }
 
 int pg_convT2d_bwd_data(const pg_conv_desc* d, int L, const float* gy, const float* w, long long w_ls, float* gx,
                         int math, void* stream) {
-  return guard([&] {
-    check_desc(d, true);
-    pg::GemmArgs a{};
-    a.kind = pg::GEMM_FPROP;
-    a.g = convT_geo(d);
-    a.L = L;
-    a.big = gy;
-    a.big_ls = big_ls(a.g);
-    a.w = w;
-    a.w_ls = w_ls;
-    a.out = gx;
-    a.out_ls = small_ls(a.g);
-    a.c_valid = d->Cin;
-    a.c_pad = a.g.CS;
-    cuda_ok(pg::launch_gemm(a, math, S(stream)), "convT2d_bwd_data");
-  });
+  OpPtrs p;
+  p.in = gy, p.w = w, p.w_ls = w_ls, p.out = gx;
+  return run_op(PG_OP_CONVT2D_BWD_DATA, d, L, p, math, stream, "convT2d_bwd_data");
 }
 
 int pg_convT2d_bwd_filter(const pg_conv_desc* d, int L, const float* x, const float* gy, float* gw, long long gw_ls,
                           int accumulate, int math, void* stream) {
-  return guard([&] {
-    check_desc(d, true);
-    pg::GemmArgs a{};
-    a.kind = pg::GEMM_WGRAD;
-    a.g = convT_geo(d);
-    a.L = L;
-    a.small = x;
-    a.small_ls = small_ls(a.g);
-    a.big = gy;
-    a.big_ls = big_ls(a.g);
-    a.out = gw;
-    a.out_ls = gw_ls;
-    a.accumulate = accumulate;
-    cuda_ok(pg::launch_gemm(a, math, S(stream)), "convT2d_bwd_filter");
-  });
+  OpPtrs p;
+  p.in = x, p.in2 = gy, p.out = gw, p.out_ls = gw_ls, p.accumulate = accumulate;
+  return run_op(PG_OP_CONVT2D_BWD_FILTER, d, L, p, math, stream, "convT2d_bwd_filter");
 }
 
 // ---------------- Dense ----------------
 int pg_dense_fwd(int L, int B, int in, int out, const float* x, const float* w, long long w_ls, const float* bias,
                  long long bias_ls, int act, float slope, float* y, int math, void* stream) {
-  return guard([&] {
-    pg::GemmArgs a{};
-    a.kind = pg::GEMM_FPROP;
-    a.g = dense_geo(B, in, out);
-    a.L = L;
-    a.big = x;
-    a.big_ls = big_ls(a.g);
-    a.w = w;
-    a.w_ls = w_ls;
-    a.out = y;
-    a.out_ls = small_ls(a.g);
-    a.bias = bias;
-    a.bias_ls = bias_ls;
-    a.act = act;
-    a.slope = slope;
-    a.c_valid = out;
-    a.c_pad = a.g.CS;
-    cuda_ok(pg::launch_gemm(a, math, S(stream)), "dense_fwd");
-  });
+  const pg_conv_desc d = dense_desc(B, in, out);
+  OpPtrs p;
+  p.in = x, p.w = w, p.w_ls = w_ls, p.bias = bias, p.bias_ls = bias_ls, p.act = act, p.slope = slope, p.out = y;
+  return run_op(PG_OP_DENSE_FWD, &d, L, p, math, stream, "dense_fwd");
 }
 
 int pg_dense_bwd_data(int L, int B, int in, int out, const float* gy, const float* w, long long w_ls, float* gx,
                       int math, void* stream) {
-  return guard([&] {
-    pg::GemmArgs a{};
-    a.kind = pg::GEMM_DGRAD;
-    a.g = dense_geo(B, in, out);
-    a.L = L;
-    a.small = gy;
-    a.small_ls = small_ls(a.g);
-    a.w = w;
-    a.w_ls = w_ls;
-    a.out = gx;
-    a.out_ls = big_ls(a.g);
-    a.c_valid = in;
-    a.c_pad = a.g.CG;
-    cuda_ok(pg::launch_gemm(a, math, S(stream)), "dense_bwd_data");
-  });
+  const pg_conv_desc d = dense_desc(B, in, out);
+  OpPtrs p;
+  p.in = gy, p.w = w, p.w_ls = w_ls, p.out = gx;
+  return run_op(PG_OP_DENSE_BWD_DATA, &d, L, p, math, stream, "dense_bwd_data");
 }
 
 int pg_dense_bwd_filter(int L, int B, int in, int out, const float* x, const float* gy, float* gw, long long gw_ls,
                         int accumulate, int math, void* stream) {
-  return guard([&] {
-    pg::GemmArgs a{};
-    a.kind = pg::GEMM_WGRAD;
-    a.g = dense_geo(B, in, out);
-    a.L = L;
-    a.small = gy;
-    a.small_ls = small_ls(a.g);
-    a.big = x;
-    a.big_ls = big_ls(a.g);
-    a.out = gw;
-    a.out_ls = gw_ls;
-    a.accumulate = accumulate;
-    cuda_ok(pg::launch_gemm(a, math, S(stream)), "dense_bwd_filter");
+  const pg_conv_desc d = dense_desc(B, in, out);
+  OpPtrs p;
+  p.in = x, p.in2 = gy, p.out = gw, p.out_ls = gw_ls, p.accumulate = accumulate;
+  return run_op(PG_OP_DENSE_BWD_FILTER, &d, L, p, math, stream, "dense_bwd_filter");
+}
+
+// ---------------- Workspace ----------------
+size_t pg_workspace_size(int op, const pg_conv_desc* d, int L, int math) {
+  size_t bytes = 0;
+  const int rc = guard([&] {
+    if (math < PG_MATH_FP32_SIMT || math > PG_MATH_TF32) throw std::invalid_argument("unknown math mode");
+    OpPtrs p;  // null device pointers pass every alignment test; strides as the arenas would have them
+    const pg::GemmArgs probe = op_args(op, d, L, p);
+    const pg::ConvGeo& g = probe.g;
+    const long long wsz = static_cast<long long>(g.CS) * g.k * g.k * g.CG;
+    p.w_ls = wsz;
+    p.bias_ls = (op % 3 == 0) ? (g.CS > g.CG ? g.CS : g.CG) : 0;
+    p.out_ls = wsz;
+    const pg::GemmWorkspace w = pg::gemm_workspace(op_args(op, d, L, p), math);
+    auto r = [](size_t f) { return (f * sizeof(float) + 255) / 256 * 256; };
+    bytes = r(w.gemm) + r(w.blo);
   });
+  return rc == PG_OK ? bytes : static_cast<size_t>(-1);
+}
+
+int pg_set_workspace(void* stream, void* workspace, size_t bytes) {
+  return guard([&] { pg::set_stream_workspace(S(stream), workspace, bytes); });
 }
 
 // ---------------- BatchNorm ----------------

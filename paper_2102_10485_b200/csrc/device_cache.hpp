@@ -57,5 +57,10 @@ enum ScratchSlot : int { SCRATCH_GEMM = 0, SCRATCH_BLO = 1, SCRATCH_SLOTS = 2 };
 float* stream_scratch(int slot, size_t floats, cudaStream_t st);
 // frees every scratch buffer of stream st (call before destroying the stream)
 void release_stream_scratch(cudaStream_t st);
+// caller-owned workspace for stream st (pg_set_workspace; nullptr detaches):
+// stream_scratch then carves its slots from it and never allocates
+void set_stream_workspace(cudaStream_t st, void* p, size_t bytes);
+// start of one GEMM call on st: resets the per-slot usage of a caller workspace
+void scratch_call_begin(cudaStream_t st);
 
 }  // namespace pg

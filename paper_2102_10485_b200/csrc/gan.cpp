@@ -275,7 +275,9 @@ void GanGroup::enqueue_step_kernels(int B, const float* real_nhwc, int par, cuda
   const int nbg = G_->blocks(), nbd = D_->blocks();
   // mask capture (parity instrumentation): segment offsets in the order G z1, D real, D fake, G z2, D fake
   const long long gsz = capture_ ? act_mask_bytes(*G_, B) : 0, dsz = capture_ ? act_mask_bytes(*D_, B) : 0;
-  const bool ov = overlap_;
+  // per-launch timing (bench.py's roofline pass) serialises the step: events
+  // around a launch would otherwise also time whatever the other stream runs
+  const bool ov = overlap_ && !gemm_timing_on();
   cudaStream_t gs = ov ? st2_ : st_;
   Trace& tg2 = ov ? tg2_ : tg_;
   if (ov) {

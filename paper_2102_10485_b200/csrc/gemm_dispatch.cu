@@ -7,6 +7,7 @@
 #include <mutex>
 #include <vector>
 #include <map>
+#include <stdexcept>
 
 #include "device_cache.hpp"
 #include "kernels.hpp"
@@ -81,10 +82,55 @@ struct ScratchBuf {
 };
 std::mutex g_scratch_mu;
 std::map<ScratchKey, ScratchBuf> g_scratch;
+
+// caller-owned workspace of a stream (pg_set_workspace): SCRATCH_GEMM is
+// carved from its start, SCRATCH_BLO from its end; both are live within one
+// GEMM call, so a request fails loudly when the two would overlap
+struct UserWs {
+  char* p = nullptr;
+  size_t bytes = 0;
+  size_t used[SCRATCH_SLOTS] = {};  // bytes requested per slot in the current GEMM call
+};
+std::map<std::pair<int, cudaStream_t>, UserWs> g_user_ws;
+size_t ws_round(size_t b) { return (b + 255) / 256 * 256; }
 }  // namespace
+
+void set_stream_workspace(cudaStream_t st, void* p, size_t bytes) {
+  std::lock_guard<std::mutex> g(g_scratch_mu);
+  const auto key = std::make_pair(cur_device(), st);
+  if (!p) {
+    g_user_ws.erase(key);
+    return;
+  }
+  if (reinterpret_cast<uintptr_t>(p) % 256) throw std::invalid_argument("workspace must be 256-byte aligned");
+  UserWs w;
+  w.p = static_cast<char*>(p);
+  w.bytes = bytes / 256 * 256;
+  g_user_ws[key] = w;
+}
+
+void scratch_call_begin(cudaStream_t st) {
+  std::lock_guard<std::mutex> g(g_scratch_mu);
+  auto it = g_user_ws.find(std::make_pair(cur_device(), st));
+  if (it != g_user_ws.end())
+    for (size_t& u : it->second.used) u = 0;
+}
 
 float* stream_scratch(int slot, size_t floats, cudaStream_t st) {
   std::lock_guard<std::mutex> g(g_scratch_mu);
+  auto uw = g_user_ws.find(std::make_pair(cur_device(), st));
+  if (uw != g_user_ws.end()) {
+    UserWs& w = uw->second;
+    const size_t need = ws_round(floats * sizeof(float));
+    size_t other = 0;
+    for (int s = 0; s < SCRATCH_SLOTS; ++s)
+      if (s != slot) other += w.used[s];
+    if (need + other > w.bytes)
+      throw std::invalid_argument("workspace too small: this call needs " + std::to_string(need + other) +
+                                  " bytes (pg_workspace_size), the stream has " + std::to_string(w.bytes));
+    w.used[slot] = need;
+    return reinterpret_cast<float*>(slot == SCRATCH_GEMM ? w.p : w.p + (w.bytes - need));
+  }
   ScratchBuf& b = g_scratch[ScratchKey{cur_device(), st, slot}];
   if (floats > b.cap) {
     if (b.p) {
@@ -105,6 +151,7 @@ float* stream_scratch(int slot, size_t floats, cudaStream_t st) {
 void release_stream_scratch(cudaStream_t st) {
   std::lock_guard<std::mutex> g(g_scratch_mu);
   const int dev = cur_device();
+  g_user_ws.erase(std::make_pair(dev, st));
   for (auto it = g_scratch.begin(); it != g_scratch.end();) {
     if (it->first.st == st && it->first.dev == dev) {
       cudaStreamSynchronize(st);
@@ -182,7 +229,21 @@ int gemm_stat_slots(const GemmArgs& a, int math, int* npack) {
   return gemm_pair_stat_slots(a, npack);
 }
 
+GemmWorkspace gemm_workspace(const GemmArgs& a, int math) {
+  GemmWorkspace w;
+  if (dense_wide_enabled() && dense_wide_supported(a)) return w;
+  if (math != MATH_FP32_SIMT && lowered_enabled(a) && gemm_lowered_supported(a)) return gemm_lowered_workspace(a, math);
+  if (math != MATH_FP32_SIMT && image_side_direct(a)) return w;
+  if (gemm_thin_supported(a)) {
+    w.gemm = gemm_thin_workspace_floats(a);
+    return w;
+  }
+  if (math != MATH_FP32_SIMT && gemm_pair_supported(a)) w.blo = gemm_pair_blo_floats(a, math);
+  return w;
+}
+
 cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
+  scratch_call_begin(st);
   if (a.stat_mode != STAT_NONE && gemm_stat_slots(a, math) == 0) return cudaErrorInvalidValue;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {

@@ -142,6 +142,23 @@ int gemm_lowered_stat_slots(const GemmArgs& a) {
   return gemm_pair_stat_slots(p);
 }
 
+GemmWorkspace gemm_lowered_workspace(const GemmArgs& a, int math) {
+  const ConvGeo& g = a.g;
+  const long long kk = (long long)g.k * g.k;
+  const long long pix = (long long)g.B * g.SH * g.SW;
+  GemmWorkspace w;
+  GemmArgs p = a.kind == GEMM_FPROP ? fprop_1x1(a, g.B, g.SH, g.SW, (int)kk * 4, g.CS)
+                                    : fprop_1x1(a, g.B, g.SH, g.SW, g.CS, (int)kk * 4);
+  p.big = p.w = p.out = reinterpret_cast<float*>(256);
+  p.big_ls = a.kind == GEMM_FPROP ? pix * kk * 4 : a.small_ls;
+  p.w_ls = a.kind == GEMM_FPROP ? a.w_ls : kk * 4 * g.CS;
+  p.out_ls = a.kind == GEMM_FPROP ? a.out_ls : pix * kk * 4;
+  w.blo = gemm_pair_blo_floats(p, math);  // the inner column GEMM on the pair engine
+  w.gemm = a.kind == GEMM_FPROP ? (size_t)(pix * kk * 4 * a.L)
+                                : (size_t)(kk * 4 * g.CS * a.L + 63) / 64 * 64 + (size_t)(pix * kk * 4 * a.L);
+  return w;
+}
+
 cudaError_t launch_gemm_lowered(const GemmArgs& a, int math, cudaStream_t st) {
   const ConvGeo& g = a.g;
   const int kk = g.k * g.k;

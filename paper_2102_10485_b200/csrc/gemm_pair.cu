@@ -1152,6 +1152,18 @@ bool blo_enabled() {
   return on;
 }
 
+// SCRATCH_BLO floats launch_gemm_pair(a, math) takes (the b_lo conditions below)
+size_t gemm_pair_blo_floats(const GemmArgs& a, int math) {
+  const ConvGeo& g = a.g;
+  if (math != MATH_TF32X3 || !blo_enabled() || atm_enabled() || !gemm_pair_supported(a)) return 0;
+  const long long kk = (long long)g.k * g.k;
+  if (a.kind == GEMM_FPROP && g.CG != 4 && pair_bn(g.CS) <= 128 && (long long)g.B * g.SH * g.SW >= 8LL * g.CS)
+    return (size_t)a.L * kk * g.CG * g.CS;
+  if (a.kind == GEMM_DGRAD && !dgrad_packed(a) && pair_bn(g.CG) <= 128 && (long long)g.B * g.GH * g.GW >= 8LL * g.CG)
+    return (size_t)a.L * g.CS * kk * g.CG;
+  return 0;
+}
+
 cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
   const ConvGeo& g = a.g;
   PairPlan P{};

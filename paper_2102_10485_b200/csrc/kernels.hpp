@@ -53,6 +53,15 @@ int gemm_stat_slots(const GemmArgs& a, int math, int* npack = nullptr);
 cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math = MATH_FP32_SIMT);
 bool gemm_thin_supported(const GemmArgs& a);
 float* gemm_scratch(size_t floats, cudaStream_t st);  // grow-only workspace for split-K reductions
+// scratch one launch_gemm(a, math) call takes from its stream, per slot
+// (SCRATCH_GEMM / SCRATCH_BLO floats); mirrors the engine choice of launch_gemm
+struct GemmWorkspace {
+  size_t gemm = 0, blo = 0;
+};
+GemmWorkspace gemm_workspace(const GemmArgs& a, int math);
+GemmWorkspace gemm_lowered_workspace(const GemmArgs& a, int math);
+size_t gemm_thin_workspace_floats(const GemmArgs& a);
+size_t gemm_pair_blo_floats(const GemmArgs& a, int math);
 // picks the engine for a math mode and problem shape
 cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st);
 

@@ -544,6 +544,12 @@ Thin classify(const GemmArgs& a) {
 
 bool gemm_thin_supported(const GemmArgs& a) { return classify(a) != T_NONE; }
 
+size_t gemm_thin_workspace_floats(const GemmArgs& a) {
+  if (classify(a) != T_IN_WGRAD) return 0;
+  const long long K = (long long)a.g.B * a.g.SH * a.g.SW;
+  return (size_t)a.L * ((K + TW_SPLIT - 1) / TW_SPLIT) * 64 * 64;
+}
+
 cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math) {
   const ConvGeo& g = a.g;
   switch (classify(a)) {

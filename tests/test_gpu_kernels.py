@@ -371,3 +371,49 @@ def test_gather_real(native, torch_cuda):
         want = data[l][idx[l]] * 2 - 1
         want[..., Cc:] = 0
         np.testing.assert_array_equal(o[l], want)
+
+
+def test_caller_owned_workspace(native, torch_cuda):
+    """pg_workspace_size / pg_set_workspace (the C-ABI never
+    allocates): the image-side shapes that need scratch run bit-identically
+    from a caller-owned buffer of exactly the reported size, and a buffer one
+    256-byte granule short fails loudly."""
+    torch = torch_cuda
+    from paper_2102_10485_b200 import _native as N
+    L, B = 2, 4
+    d = N.ConvDesc(B=B, Cin=3, H=64, W=64, Cout=64, OH=32, OW=32, k=4, s=2, p=1)
+    dT = N.ConvDesc(B=B, Cin=64, H=32, W=32, Cout=3, OH=64, OW=64, k=4, s=2, p=1)
+    g = torch.Generator().manual_seed(5)
+    big = torch.randn(L, B * 64 * 64 * 4, generator=g).cuda()
+    small = torch.randn(L, B * 32 * 32 * 64, generator=g).cuda()
+    w = (0.02 * torch.randn(L, 64 * 16 * 4, generator=g)).cuda()
+    bias = torch.zeros(L, 4).cuda()
+    runs = {
+        N.PG_OP_CONV2D_BWD_FILTER: (d, lambda out: native.pg_conv2d_bwd_filter(
+            C.byref(d), L, ptr(big), ptr(small), ptr(out), out.shape[1], 0, N.MATH_TF32X3, None), 64 * 16 * 4),
+        N.PG_OP_CONVT2D_FWD: (dT, lambda out: native.pg_convT2d_fwd(
+            C.byref(dT), L, ptr(small), ptr(w), w.shape[1], ptr(bias), 4, N.ACT_TANH, 0.0, ptr(out),
+            N.MATH_TF32X3, None), B * 64 * 64 * 4),
+        N.PG_OP_CONV2D_BWD_DATA: (d, lambda out: native.pg_conv2d_bwd_data(
+            C.byref(d), L, ptr(small), ptr(w), w.shape[1], ptr(out), N.MATH_TF32X3, None), B * 64 * 64 * 4),
+    }
+    try:
+        for op, (desc, run, n_out) in runs.items():
+            ref = torch.zeros(L, n_out).cuda()
+            N.check(run(ref), "ws")
+            need = native.pg_workspace_size(op, C.byref(desc), L, N.MATH_TF32X3)
+            assert 0 < need < (1 << 40), (op, need)
+            ws = torch.empty(need // 4 + 64, dtype=torch.float32, device="cuda")
+            base = (ws.data_ptr() + 255) // 256 * 256
+            N.check(native.pg_set_workspace(None, C.c_void_p(base), need), "ws")
+            out = torch.zeros(L, n_out).cuda()
+            N.check(run(out), "ws")
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref), op
+            N.check(native.pg_set_workspace(None, C.c_void_p(base), need - 256), "ws")
+            rc = run(torch.zeros(L, n_out).cuda())
+            assert rc == N.PG_EINVAL and b"workspace too small" in native.pg_last_error(), op
+            N.check(native.pg_set_workspace(None, None, 0), "ws")
+            del ws
+    finally:
+        native.pg_set_workspace(None, None, 0)
