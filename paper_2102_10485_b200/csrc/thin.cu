@@ -588,13 +588,18 @@ cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math) {
       const int nchunk = (int)((K + TW_SPLIT - 1) / TW_SPLIT);
       float* part = gemm_scratch((size_t)a.L * nchunk * 64 * 64, st);
       if (!part) return cudaErrorMemoryAllocation;
-      if (math == MATH_TF32X3)
-        thin_in_wgrad_mma_kernel<true><<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
-      else if (math == MATH_TF32)
-        thin_in_wgrad_mma_kernel<false><<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
-      else
-        thin_in_wgrad_partial_kernel<<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
-      cudaError_t e = launched();
+      cudaError_t e;
+      if (wgrad4_supported(a, math)) {
+        e = launch_wgrad4(a, math, part, nchunk, st);  // tcgen05 (wgrad4.cu)
+      } else {
+        if (math == MATH_TF32X3)
+          thin_in_wgrad_mma_kernel<true><<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
+        else if (math == MATH_TF32)
+          thin_in_wgrad_mma_kernel<false><<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
+        else
+          thin_in_wgrad_partial_kernel<<<dim3(nchunk, a.L), 256, 0, st>>>(a, part, nchunk);
+        e = launched();
+      }
       if (e != cudaSuccess) return e;
       const int nout = g.CS * g.k * g.k * 4;
       thin_in_wgrad_reduce_kernel<<<dim3((nout + 255) / 256, a.L), 256, 0, st>>>(a, part, nchunk);

@@ -20,6 +20,7 @@ p.add_argument("--labels", type=int, default=125)
 p.add_argument("--batch", type=int, default=32)
 p.add_argument("--math", default="tf32x3")
 p.add_argument("--iters", type=int, default=5)
+p.add_argument("--save", default="", help="write the op output (.npy) for A/B comparisons")
 args = p.parse_args()
 math = {"fp32": 0, "tf32x3": 1, "tf32": 2}[args.math]
 cin, cout, h = {1: (3, 64, 64), 2: (64, 128, 32), 3: (128, 256, 16), 4: (256, 512, 8)}[args.layer]
@@ -27,6 +28,7 @@ pad = lambda c: (c + 3) // 4 * 4
 L, B = args.labels, args.batch
 oh = h // 2
 d = N.ConvDesc(B=B, Cin=cin, H=h, W=h, Cout=cout, OH=oh, OW=oh, k=4, s=2, p=1)
+torch.manual_seed(0)
 x = torch.randn(L, B, h, h, pad(cin), device="cuda")
 gy = torch.randn(L, B, oh, oh, pad(cout), device="cuda")
 wl = pad(cout) * 16 * pad(cin)
@@ -61,3 +63,8 @@ ms = e0.elapsed_time(e1) / args.iters
 flops = 2.0 * L * B * oh * oh * cout * cin * 16
 print(f"{args.op} layer {args.layer} ({cin}->{cout}, {h}x{h}) L={L} B={B} math={args.math}: {ms:.3f} ms, "
       f"{flops / ms / 1e9:.1f} TFLOP/s algorithmic")
+if args.save:
+    import numpy as np
+    torch.manual_seed(0)
+    out = {"conv_fwd": y, "conv_dgrad": gx}.get(args.op, gw)
+    np.save(args.save, out.cpu().numpy())
