@@ -254,7 +254,8 @@ cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
   cudaError_t r;
   if (dense_wide_enabled() && dense_wide_supported(a)) r = launch_dense_wide(a, st);  // latent projection
   else if (math != MATH_FP32_SIMT && lowered_enabled(a) && gemm_lowered_supported(a)) r = launch_gemm_lowered(a, math, st);
-  else if (math != MATH_FP32_SIMT && image_side_direct(a)) r = launch_gemm_pair(a, math, st);  // 4-channel FPROP
+  else if (math != MATH_FP32_SIMT && fprop4_supported(a, math)) r = launch_fprop4(a, math, st);  // 4-channel FPROP
+  else if (math != MATH_FP32_SIMT && image_side_direct(a)) r = launch_gemm_pair(a, math, st);  // 4-channel FPROP + stats
   else if (gemm_thin_supported(a)) r = launch_gemm_thin(a, st, math);  // image-side / dense-head shapes
   else if (math != MATH_FP32_SIMT && gemm_pair_supported(a)) r = launch_gemm_pair(a, math, st);  // big conv GEMMs
   else if (math != MATH_FP32_SIMT && gemm_tma_supported(a)) r = launch_gemm_tma(a, math, st);  // conv GEMMs

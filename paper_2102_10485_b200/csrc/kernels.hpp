@@ -52,6 +52,9 @@ int gemm_stat_slots(const GemmArgs& a, int math, int* npack = nullptr);
 // thin.cu; math selects the 4-channel weight gradient's form (TF32 modes: mma.sync tensor cores)
 cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math = MATH_FP32_SIMT);
 bool gemm_thin_supported(const GemmArgs& a);
+// fprop4.cu: the 4-channel FPROP (CS = 64, k = 4, no fused statistics) on tcgen05, A gathered into TMEM
+bool fprop4_supported(const GemmArgs& a, int math);
+cudaError_t launch_fprop4(const GemmArgs& a, int math, cudaStream_t st);
 // wgrad4.cu: the 4-channel weight gradient (CS = 64, k = 4) on tcgen05; part = thin.cu's split-K scratch
 bool wgrad4_supported(const GemmArgs& a, int math);
 cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, cudaStream_t st);
