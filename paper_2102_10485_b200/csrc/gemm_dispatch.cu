@@ -232,6 +232,7 @@ int gemm_stat_slots(const GemmArgs& a, int math, int* npack) {
 GemmWorkspace gemm_workspace(const GemmArgs& a, int math) {
   GemmWorkspace w;
   if (dense_wide_enabled() && dense_wide_supported(a)) return w;
+  if (math != MATH_FP32_SIMT && dgrad4_supported(a, math)) return w;
   if (math != MATH_FP32_SIMT && lowered_enabled(a) && gemm_lowered_supported(a)) return gemm_lowered_workspace(a, math);
   if (math != MATH_FP32_SIMT && image_side_direct(a)) return w;
   if (gemm_thin_supported(a)) {
@@ -253,6 +254,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
   }
   cudaError_t r;
   if (dense_wide_enabled() && dense_wide_supported(a)) r = launch_dense_wide(a, st);  // latent projection
+  else if (math != MATH_FP32_SIMT && dgrad4_supported(a, math)) r = launch_dgrad4(a, math, st);  // 4-channel DGRAD
   else if (math != MATH_FP32_SIMT && lowered_enabled(a) && gemm_lowered_supported(a)) r = launch_gemm_lowered(a, math, st);
   else if (math != MATH_FP32_SIMT && fprop4_supported(a, math)) r = launch_fprop4(a, math, st);  // 4-channel FPROP
   else if (math != MATH_FP32_SIMT && image_side_direct(a)) r = launch_gemm_pair(a, math, st);  // 4-channel FPROP + stats

@@ -55,6 +55,9 @@ bool gemm_thin_supported(const GemmArgs& a);
 // fprop4.cu: the 4-channel FPROP (CS = 64, k = 4, no fused statistics) on tcgen05, A gathered into TMEM
 bool fprop4_supported(const GemmArgs& a, int math);
 cudaError_t launch_fprop4(const GemmArgs& a, int math, cudaStream_t st);
+// dgrad4.cu: the 4-channel DGRAD (CS = 64, k4 s2 p1, no fused statistics) on tcgen05, phase-packed N = 16
+bool dgrad4_supported(const GemmArgs& a, int math);
+cudaError_t launch_dgrad4(const GemmArgs& a, int math, cudaStream_t st);
 // wgrad4.cu: the 4-channel weight gradient (CS = 64, k = 4) on tcgen05; part = thin.cu's split-K scratch
 bool wgrad4_supported(const GemmArgs& a, int math);
 cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, cudaStream_t st);

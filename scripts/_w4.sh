@@ -1,6 +1,5 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-(timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "conv2d or convT2d" -p no:cacheprovider 2>&1 | tail -2) > gpurun_out/f4_tests.log
-for v in 0 1; do PG_FPROP4=$v timeout 300 python scripts/gemm_bench.py --op conv_fwd --layer 1 --iters 20 --save gpurun_out/f4_$v.npy; done > gpurun_out/f4_bench.log 2>&1
-python scripts/ab_compare.py gpurun_out/f4_1.npy gpurun_out/f4_0.npy >> gpurun_out/f4_bench.log 2>&1
-rm -f gpurun_out/*.npy
-cat gpurun_out/f4_tests.log gpurun_out/f4_bench.log
+timeout 1500 python -m pytest tests -q -m gpu -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; tail -2 gpurun_out/bench.log | cut -c1-600
