@@ -72,7 +72,6 @@ struct D4Plan {
   float slope;
   int c_valid, c_pad;
   int box_bytes;     // TMA bytes of one patch half
-  int dbg;           // PG_D4_DBG (timing diagnostics; wrong results): 1 no TMEM stores, 2 no MMAs, 3 no output stores, 4 no patch reads
 };
 
 PG_DEV void mma_tf32_ts1(uint32_t tmem_d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
@@ -83,12 +82,41 @@ PG_DEV void mma_tf32_ts1(uint32_t tmem_d, uint32_t a_tmem, uint64_t bdesc, uint3
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-PG_DEV float d4_act(int act, float x, float slope) {
-  if (act == ACT_RELU) return x > 0.f ? x : 0.f;
-  if (act == ACT_LRELU) return x >= 0.f ? x : x * slope;
-  if (act == ACT_TANH) return tanhf(x);
-  if (act == ACT_SIGMOID) return 1.f / (expf(-x) + 1.f);
+template <int ACT>
+PG_DEV float d4_act(float x, float slope) {
+  if (ACT == ACT_RELU) return x > 0.f ? x : 0.f;
+  if (ACT == ACT_LRELU) return x >= 0.f ? x : x * slope;
+  if (ACT == ACT_TANH) return tanhf(x);
+  if (ACT == ACT_SIGMOID) return 1.f / (expf(-x) + 1.f);
   return x;
+}
+
+// the four output pixels (2 bi - 1 + ry, 2 bj - 1 + rx) of base position (bi, bj):
+// bias + activation on the valid channels, zeros in the pad channels
+template <int ACT>
+PG_DEV void d4_store(const float (&sum)[16], const D4Plan& P, int label, int b, int bi, int bj) {
+  const ConvGeo& g = P.g;
+  const float* bias = P.bias ? P.bias + (long long)label * P.bias_ls : nullptr;
+  float bb[4] = {0.f, 0.f, 0.f, 0.f};
+  if (bias)
+    for (int c = 0; c < 4 && c < P.c_valid; ++c) bb[c] = __ldg(bias + c);
+  float* ob = P.out + (long long)label * P.out_ls + (long long)b * g.GH * g.GW * 4;
+#pragma unroll
+  for (int ry = 0; ry < 2; ++ry) {
+    const int y = 2 * bi - 1 + ry, x0 = 2 * bj - 1;
+    if (y < 0 || y >= g.GH) continue;
+    float* orow = ob + ((long long)y * g.GW) * 4;
+#pragma unroll
+    for (int rx = 0; rx < 2; ++rx) {
+      const int x = x0 + rx;
+      if (x < 0 || x >= g.GW) continue;
+      const int n0 = (ry * 2 + rx) * 4;
+      float o[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[c] = c % P.c_pad < P.c_valid ? d4_act<ACT>(sum[n0 + c] + bb[c], P.slope) : 0.f;
+      *reinterpret_cast<float4*>(orow + x * 4) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
 }
 
 // first base position and base row of tile t (of its image)
@@ -155,10 +183,6 @@ __global__ void __launch_bounds__(D4_NT, 1)
         d4_tile(P, t, label, b, p0, ib0);
         const int ps = i % D4_PS;
         mbar_wait(pfree + ps, ((i / D4_PS) & 1) ^ 1);
-        if (P.dbg == 5) {  // diagnostics: no patch loads
-          mbar_arrive(pfull + ps);
-          continue;
-        }
         mbar_expect_tx(pfull + ps, 2 * P.box_bytes);
         const uint32_t dst = smem_u32(smem + ps * D4_PATCH);
         tma_load_5d(dst, &tmS, pfull + ps, 0, -1, ib0 - 1, b, label);  // P.prows x P.pcols pixels
@@ -213,7 +237,7 @@ __global__ void __launch_bounds__(D4_NT, 1)
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float4 v = P.dbg == 4 ? make_float4(1.f, 2.f, 3.f, 4.f) : *reinterpret_cast<const float4*>(row + ((c ^ (idx & 7)) << 4));
+          const float4 v = *reinterpret_cast<const float4*>(row + ((c ^ (idx & 7)) << 4));
           const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int uu = 0; uu < 4; ++uu) {
@@ -229,10 +253,8 @@ __global__ void __launch_bounds__(D4_NT, 1)
         mbar_wait(afree + as, ((kit / D4_AS) & 1) ^ 1);
         tc_fence_after();
         const uint32_t ta = tmem + lane_off + as * 64;
-        if (P.dbg != 1) {
-          tmem_st32(ta, hi);
-          if (X3) tmem_st32(ta + 32, lo);
-        }
+        tmem_st32(ta, hi);
+        if (X3) tmem_st32(ta + 32, lo);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -274,8 +296,7 @@ __global__ void __launch_bounds__(D4_NT, 1)
             const int ai = ((kb & 1) * 4 + kk) % D4_NACC;
             const uint32_t d = d0 + ai * 16;
             const uint32_t acc = (kb * 4 + kk) >= D4_NACC ? 1u : 0u;
-            if (P.dbg == 2) {
-            } else if (X3) {
+            if (X3) {
               mma_tf32_ts1(d, a_t + 32, bh0 + bofs, idesc, acc);  // small terms first
               mma_tf32_ts1(d, a_t, bl0 + bofs, idesc, 1u);
               mma_tf32_ts1(d, a_t, bh0 + bofs, idesc, 1u);
@@ -314,32 +335,14 @@ __global__ void __launch_bounds__(D4_NT, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(accfree + buf);
       const int pos = p0 + r;
-      if (pos >= nbase || P.dbg == 3) continue;
+      if (pos >= nbase) continue;
       const int bi = pos / P.gw1, bj = pos % P.gw1;
-      const float* bias = P.bias ? P.bias + (long long)label * P.bias_ls : nullptr;
-      float bb[4] = {0.f, 0.f, 0.f, 0.f};
-      if (bias)
-        for (int c = 0; c < 4 && c < P.c_valid; ++c) bb[c] = __ldg(bias + c);
-      float o[16];
-#pragma unroll
-      for (int n = 0; n < 16; ++n) {
-        const int c = n & 3;
-        const float x = d4_act(P.act, sum[n] + bb[c], P.slope);
-        o[n] = c % P.c_pad < P.c_valid ? x : 0.f;
-      }
-      float* ob = P.out + (long long)label * P.out_ls + (long long)b * g.GH * g.GW * 4;
-#pragma unroll
-      for (int ry = 0; ry < 2; ++ry) {
-        const int y = 2 * bi - 1 + ry, x0 = 2 * bj - 1;
-        if (y < 0 || y >= g.GH) continue;
-        float* orow = ob + ((long long)y * g.GW) * 4;
-#pragma unroll
-        for (int rx = 0; rx < 2; ++rx) {
-          const int x = x0 + rx;
-          if (x < 0 || x >= g.GW) continue;
-          const int n0 = (ry * 2 + rx) * 4;
-          *reinterpret_cast<float4*>(orow + x * 4) = make_float4(o[n0], o[n0 + 1], o[n0 + 2], o[n0 + 3]);
-        }
+      switch (P.act) {  // one specialised epilogue per activation (tanh only on the valid channels)
+        case ACT_TANH: d4_store<ACT_TANH>(sum, P, label, b, bi, bj); break;
+        case ACT_RELU: d4_store<ACT_RELU>(sum, P, label, b, bi, bj); break;
+        case ACT_LRELU: d4_store<ACT_LRELU>(sum, P, label, b, bi, bj); break;
+        case ACT_SIGMOID: d4_store<ACT_SIGMOID>(sum, P, label, b, bi, bj); break;
+        default: d4_store<ACT_NONE>(sum, P, label, b, bi, bj); break;
       }
     }
   }
@@ -393,7 +396,6 @@ cudaError_t launch_dgrad4(const GemmArgs& a, int math, cudaStream_t st) {
   P.c_pad = a.c_pad;
   P.prows = (D4_TILE - 1) / P.gw1 + 3;
   P.box_bytes = 32 * 4 * P.pcols * P.prows;
-  if (const char* e = std::getenv("PG_D4_DBG")) P.dbg = std::atoi(e);
   CUtensorMap ts;
   const long long sd[5] = {g.CS, g.SW, g.SH, g.B, a.L};
   const long long ss[4] = {g.CS, (long long)g.SW * g.CS, (long long)g.SH * g.SW * g.CS, a.small_ls};

@@ -70,7 +70,6 @@ struct W4Plan {
   long long big_ls;
   float* part;
   int patch_rows, patch_bytes;  // patch mode: input rows per k-block, TMA bytes of the patch box
-  int dbg;  // PG_W4_DBG (diagnostics): 1 drain pattern, 2 B = 1, 3 A = B = 1
 };
 
 PG_DEV int chunk_kblocks(const W4Plan& P, int chunk) {
@@ -217,7 +216,6 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        if (P.dbg >= 2) cur[i] = make_float4(1.f, 1.f, 1.f, 1.f);
         const float e4[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
         int tap, px;
         elem(i, tap, px);
@@ -229,16 +227,11 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
           if (X3) bl[off] = e4[c4] - tf32_trunc(e4[c4]);
         }
       }
-      if (P.dbg == 3) {
-        float4* aw = reinterpret_cast<float4*>(smem + s * W4_TS);
-#pragma unroll
-        for (int i = 0; i < W4_A / 16 / 64; ++i) aw[gt + 64 * i] = make_float4(1.f, 1.f, 1.f, 1.f);
-      }
       if (X3) {
         float4* al = reinterpret_cast<float4*>(ops + o * W4_OS);
 #pragma unroll
         for (int i = 0; i < W4_A / 16 / 64; ++i) {
-          const float4 a = P.dbg == 3 ? make_float4(1.f, 1.f, 1.f, 1.f) : a4[i];
+          const float4 a = a4[i];
           al[gt + 64 * i] =
               make_float4(a.x - tf32_trunc(a.x), a.y - tf32_trunc(a.y), a.z - tf32_trunc(a.z), a.w - tf32_trunc(a.w));
         }
@@ -310,7 +303,7 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
           tmem_ld32(tmem + lane_base + buf * 64 + c * 32, r);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc[c * 32 + i] += P.dbg == 1 ? (float)(row * 100 + c * 32 + i) : __uint_as_float(r[i]);
+          for (int i = 0; i < 32; ++i) acc[c * 32 + i] += __uint_as_float(r[i]);
         }
         tc_fence_before();
         __syncwarp();
@@ -357,7 +350,6 @@ cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, 
   P.big = a.big;
   P.big_ls = a.big_ls;
   P.part = part;
-  if (const char* e = std::getenv("PG_W4_DBG")) P.dbg = std::atoi(e);
   CUtensorMap tm;
   const long long dims[3] = {g.CS, P.K, a.L};
   const long long strides[2] = {g.CS, a.small_ls};

@@ -2,7 +2,7 @@
 (device-resident random data), CUDA-event timed; used for ncu captures.
   python scripts/gemm_bench.py --op conv_fwd --layer 2 [--math tf32x3] [--iters 5]
 layers (c4 discriminator, 125 labels x batch 32): 1 = 3->64 64x64, 2 = 64->128 32x32,
-3 = 128->256 16x16, 4 = 256->512 8x8; ops: conv_fwd, conv_dgrad, conv_wgrad."""
+3 = 128->256 16x16, 4 = 256->512 8x8; ops: conv_fwd, conv_dgrad, conv_wgrad, convt_fwd (the generator layer mirroring it)."""
 import argparse
 import ctypes as C
 import os
@@ -37,6 +37,9 @@ bias = torch.zeros(L, pad(cout), device="cuda")
 y = torch.empty(L, B, oh, oh, pad(cout), device="cuda")
 gx = torch.empty_like(x)
 gw = torch.empty_like(w)
+dT = N.ConvDesc(B=B, Cin=cout, H=oh, W=oh, Cout=cin, OH=h, OW=h, k=4, s=2, p=1)
+wT = torch.randn(L, wl, device="cuda") * 0.02
+biasT = torch.zeros(L, pad(cin), device="cuda")
 lib = N.lib()
 P = lambda t: C.c_void_p(t.data_ptr())
 
@@ -46,6 +49,9 @@ def run():
         N.check(lib.pg_conv2d_fwd(C.byref(d), L, P(x), P(w), wl, P(bias), pad(cout), 0, 0.0, P(y), math, None))
     elif args.op == "conv_dgrad":
         N.check(lib.pg_conv2d_bwd_data(C.byref(d), L, P(gy), P(w), wl, P(gx), math, None))
+    elif args.op == "convt_fwd":  # the generator's mirror layer: cout -> cin channels, oh -> h (tanh on layer 1)
+        N.check(lib.pg_convT2d_fwd(C.byref(dT), L, P(gy), P(wT), wl, P(biasT), pad(cin), 3 if args.layer == 1 else 1,
+                                   0.0, P(gx), math, None))
     else:
         N.check(lib.pg_conv2d_bwd_filter(C.byref(d), L, P(x), P(gy), P(gw), wl, 0, math, None))
 
@@ -66,5 +72,5 @@ print(f"{args.op} layer {args.layer} ({cin}->{cout}, {h}x{h}) L={L} B={B} math={
 if args.save:
     import numpy as np
     torch.manual_seed(0)
-    out = {"conv_fwd": y, "conv_dgrad": gx}.get(args.op, gw)
+    out = {"conv_fwd": y, "conv_dgrad": gx, "convt_fwd": gx}.get(args.op, gw)
     np.save(args.save, out.cpu().numpy())

@@ -10,7 +10,8 @@ from collections import defaultdict
 
 path, steps, tag = sys.argv[1], float(sys.argv[2]), sys.argv[3]
 GEMM = ("gemm_pair_kernel", "gemm_tc_kernel", "gemm_tma_kernel", "gemm_simt_kernel", "thin_", "dense_wide",
-        "dense_fprop", "dense_dgrad", "dense_wgrad", "col2im4", "im2col4", "wt_transpose4", "tf32_lo")
+        "dense_fprop", "dense_dgrad", "dense_wgrad", "col2im4", "im2col4", "wt_transpose4", "tf32_lo",
+        "fprop4_kernel", "wgrad4_kernel", "dgrad4_kernel")
 with open(path) as f:
     rows = list(csv.DictReader(ln for ln in f if ln.startswith('"')))
 per = defaultdict(float)
