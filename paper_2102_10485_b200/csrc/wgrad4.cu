@@ -5,29 +5,29 @@
 // K = the B*SH*SW small-map pixels of a label (network.cpp:121, the conv_bwd
 // weight-gradient GEMM; ConvT uses the same GEMM with the roles swapped).
 //
-// Round 1 ran this on warp-level mma.sync (thin.cu, 0.8 ms per c4 launch
-// against a 0.2 ms HBM floor).  Here one CTA per SM walks (label, 1024-pixel
+// Round 1 ran this on warp-level mma.sync (thin.cu, 0.77 ms per c4 launch
+// against a 0.20 ms HBM floor).  Here one CTA per SM walks (label, 1024-pixel
 // chunk) work items; a chunk's 32 k-blocks of 32 pixels feed
-// `tcgen05.mma.cta_group::1.kind::tf32` with M = 128, N = 64, K = 8:
-//   A = gy^T (M = cs, MN-major): two TMA boxes {32 cs, 32 pixels} per k-block
-//       in the 128B_ATOM_32B swizzle (the pair engine's MN-major layout); rows
-//       64..127 of the M = 128 MMA read the stage's B bytes and land in TMEM
-//       lanes no warp reads (tcgen05 has no M = 64 layout that keeps one row per
-//       lane in a single lane quarter pair; the half-empty tile costs tensor
-//       time the HBM-bound kernel has to spare)
-//   B = im2col(x) (N = tap x 4 channels, K-major, 128-byte swizzle): the
-//       gather warps read each tap's 16-byte pixel from global memory
-//       (L1/L2-resident: a k-block touches ~4 input rows) and scatter its four
-//       channels into the rows n = tap * 4 + c -- no 16-byte TMA boxes (512
-//       tiny rows per k-block); in TF32X3 they also write lo = x - trunc(x) of
-//       A and B into the lo ring (3xTF32: a_lo b_hi + a_hi b_lo + a_hi b_hi)
-// TMEM: two 64-column accumulation buffers; a segment of 8 k-blocks (96 MMA
-// adds) is drained into fp32 registers (gemm_pair.cu's accuracy design) and a
-// chunk's 64 x 64 partial goes to the split-K scratch that thin.cu's fixed-order
-// reduce sums (deterministic, no atomics).
-//
-// Warp roles (384 threads): warps 0-1 drain (TMEM lane quarters 0, 1 = rows
-// 0..63), warp 2 TMA, warp 3 TMEM allocation + MMA issue, warps 4-11 gather.
+// `tcgen05.mma.cta_group::1.kind::tf32` in the TS form, M = 128, N = 64, K = 8:
+//   A = gy^T (M = gradient channel): one TMA box {64 channels, 32 pixels} per
+//       k-block (plain 256-byte rows); four "A warps" (lane quarters 0, 1; even
+//       and odd k-blocks) read a channel column each and write its hi / lo
+//       into a tensor-memory ring.  TMEM lanes 64..127 are never written: the
+//       M = 128 MMA's upper half is discarded (tcgen05 costs an M = 64 MMA
+//       the same issue slots), which bounds the kernel at ~50% tensor use
+//   B = im2col(x) (N = tap x 4 channels, K-major, 128-byte swizzle): the input
+//       rows under the k-block arrive as one TMA box next to gy; four groups
+//       of two gather warps (one k-block each in flight) read each tap's
+//       16-byte pixel from that patch and scatter its channels into the rows
+//       n = tap * 4 + c (+ lo parts in TF32X3) of an operand ring
+// 3xTF32: a_lo b_hi + a_hi b_lo + a_hi b_hi.  TMEM: the A ring, then two
+// 64-column accumulation buffers; a segment of 8 k-blocks (96 MMA adds) is
+// drained into fp32 registers (gemm_pair.cu's accuracy design) and a chunk's
+// 64 x 64 partial goes to the split-K scratch that thin.cu's fixed-order
+// reduce sums (deterministic, no atomics).  Measured steps (c4, per launch):
+// SS form with A and A lo in shared memory 0.46 ms (shared-memory bound: the
+// M = 128 MMA read 48 KB of A per k-block), this TS form 0.44 ms with the
+// tensor pipe 46% busy; two accumulation chains per segment: no change.
 #include <cuda.h>
 #include <stdint.h>
 
@@ -44,23 +44,24 @@ namespace {
 
 using namespace tmac;
 
-constexpr int W4_T = 8;          // TMA ring: gy boxes + x patch (DRAM latency in flight)
-constexpr int W4_O = 4;          // operand ring: B hi, A lo, B lo (gather -> MMA)
+constexpr int W4_T = 6;          // TMA ring: gy tile + x patch (DRAM latency in flight)
+constexpr int W4_O = 8;          // operand ring: B hi, B lo (gather -> MMA)
+constexpr int W4_AS = 4;         // TMEM A ring: gy^T hi / lo (A warps -> MMA)
 constexpr int W4_KB = 32;        // pixels per k-block
 constexpr int W4_KSEG = 8;       // k-blocks per TMEM accumulation segment
 constexpr int W4_CHUNK = 1024;   // pixels per work item (thin.cu TW_SPLIT: same partial layout)
-constexpr int W4_NG = 8;         // gather warps
-constexpr int W4_NGRP = 4;       // gather groups (k-blocks in flight), W4_NG / W4_NGRP warps each
-constexpr int W4_NT = (4 + W4_NG) * 32;
-constexpr int W4_A = 2 * 4096;   // A stage: 2 MN atoms of 32 cs x 32 pixels
-constexpr int W4_B = 16 * 512;   // B stage: 16 taps x 32 pixels x 16 B
-constexpr int W4_PATCH = 4096;  // input rows of a k-block (patch mode)
-constexpr int W4_TS = W4_A + W4_PATCH;   // TMA slot: A hi | x patch
-constexpr int W4_OS = W4_A + 2 * W4_B;   // operand slot: A lo | B lo | B hi
-// the M = 128 MMA reads A rows 64..127 at +8 KB / +12 KB: inside the next
-// slot (or the pad after the last one) for A hi, the B lo part for A lo
-constexpr int W4_TPAD = 2 * 4096 - W4_PATCH;
-constexpr int W4_SMEM = W4_T * W4_TS + W4_TPAD + W4_O * W4_OS + 1024 + 1024;
+constexpr int W4_NGRP = 4;       // gather groups of two warps (k-blocks in flight)
+constexpr int W4_NT = 16 * 32;
+constexpr int W4_A = 64 * 32 * 4;  // gy tile: 32 pixel rows x 64 channels (plain, 256 B rows)
+constexpr int W4_B = 16 * 512;     // B operand: 64 rows (tap, channel) x 32 pixels, K-major SW128
+constexpr int W4_PATCH = 4096;     // input rows of a k-block (patch mode)
+constexpr int W4_TS = W4_A + W4_PATCH;  // TMA slot: gy tile | x patch
+constexpr int W4_OS = 2 * W4_B;         // operand slot: B lo | B hi
+constexpr int W4_SMEM = W4_T * W4_TS + W4_O * W4_OS + 1024 + 1024;
+constexpr uint32_t W4_ACOL = W4_AS * 64;  // accumulators after the A ring: 2 segments x W4_NACC x 64 columns
+#ifndef W4_NACC
+#define W4_NACC 1  // (2 measured no faster) independent accumulation chains per segment (MMA kk -> kk % W4_NACC), summed by the drain
+#endif
 
 struct W4Plan {
   ConvGeo g;
@@ -78,17 +79,31 @@ PG_DEV int chunk_kblocks(const W4Plan& P, int chunk) {
   return (int)((px + W4_KB - 1) / W4_KB);
 }
 
+PG_DEV void mma_tf32_ts_w4(uint32_t tmem_d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Warp roles (512 threads): 0-1 drain (TMEM lane quarters 0, 1 = gradient
+// channels 0..63), 2 TMA, 3 TMEM allocation + MMA issue, 4-5 and 8-9 A warps
+// (quarters 0, 1; even / odd k-blocks), 6-7 and 10-15 gather (four groups of
+// two warps, k-block it % 4 each).
 template <bool X3, bool PATCH>
-__global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
-                                                         const W4Plan P) {
+__global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                         const __grid_constant__ CUtensorMap tmX, const W4Plan P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* ops = smem + W4_T * W4_TS + W4_TPAD;
+  uint8_t* ops = smem + W4_T * W4_TS;
   uint64_t* full = reinterpret_cast<uint64_t*>(ops + W4_O * W4_OS);
   uint64_t* tfree = full + W4_T;
   uint64_t* ready = tfree + W4_T;
   uint64_t* ofree = ready + W4_O;
-  uint64_t* seg_full = ofree + W4_O;
+  uint64_t* aready = ofree + W4_O;
+  uint64_t* afree = aready + W4_AS;
+  uint64_t* seg_full = afree + W4_AS;
   uint64_t* seg_empty = seg_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(seg_empty + 2);
 
@@ -98,11 +113,15 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
   if (tid == 0) {
     for (int s = 0; s < W4_T; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(tfree + s, 1);
+      mbar_init(tfree + s, 4);  // the k-block's two A warps and two gather warps read the slot
     }
     for (int s = 0; s < W4_O; ++s) {
-      mbar_init(ready + s, W4_NG / W4_NGRP);
+      mbar_init(ready + s, 2);
       mbar_init(ofree + s, 1);
+    }
+    for (int s = 0; s < W4_AS; ++s) {
+      mbar_init(aready + s, 2);
+      mbar_init(afree + s, 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(seg_full + b, 1);
@@ -110,66 +129,88 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
     }
     fence_barrier_init();
   }
-  if (warp == 3) tmem_alloc(tmem_slot, 128);
+  if (warp == 3) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  struct Cur {
+    int t, kb, nkb;
+  };
+  auto start_at = [&](int t) { return Cur{t, 0, t < nitems ? chunk_kblocks(P, t % P.nchunk) : 0}; };
+  auto adv = [&](Cur& c) {
+    if (++c.kb >= c.nkb) c = start_at(c.t + (int)gridDim.x);
+  };
+
   if (warp == 2) {
-    // ===================== TMA: gy boxes =====================
+    // ===================== TMA: gy tile (+ x patch) per k-block =====================
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       if (PATCH) tma_prefetch_desc(&tmX);
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
-        const int l = t / P.nchunk, chunk = t % P.nchunk;
-        const int nkb = chunk_kblocks(P, chunk);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % W4_T;
-          mbar_wait(tfree + s, ((it / W4_T) & 1) ^ 1);
-          mbar_expect_tx(full + s, W4_A + (PATCH ? P.patch_bytes : 0));
-          const int p0 = chunk * W4_CHUNK + kb * W4_KB;
-          const uint32_t dst = smem_u32(smem + s * W4_TS);
-          tma_load_3d(dst, &tmA, full + s, 0, p0, l);
-          tma_load_3d(dst + 4096, &tmA, full + s, 32, p0, l);
-          if (PATCH) {  // the input rows under the k-block's 32 / SW output rows of image b
-            const int r = p0 / g.SW;
-            tma_load_4d(dst + W4_A, &tmX, full + s, 0, (r % g.SH) * g.s - g.p, r / g.SH, l);
-          }
+      for (Cur c = start_at(blockIdx.x); c.t < nitems; adv(c), ++it) {
+        const int l = c.t / P.nchunk, chunk = c.t % P.nchunk;
+        const int s = it % W4_T;
+        mbar_wait(tfree + s, ((it / W4_T) & 1) ^ 1);
+        mbar_expect_tx(full + s, W4_A + (PATCH ? P.patch_bytes : 0));
+        const int p0 = chunk * W4_CHUNK + c.kb * W4_KB;
+        const uint32_t dst = smem_u32(smem + s * W4_TS);
+        tma_load_3d(dst, &tmA, full + s, 0, p0, l);
+        if (PATCH) {  // the input rows under the k-block's 32 / SW output rows of image b
+          const int r = p0 / g.SW;
+          tma_load_4d(dst + W4_A, &tmX, full + s, 0, (r % g.SH) * g.s - g.p, r / g.SH, l);
         }
       }
     }
-  } else if (warp >= 4) {
-    // ===================== gather: B = im2col(x) (+ lo parts) =====================
+  } else if (warp == 4 || warp == 5 || warp == 8 || warp == 9) {
+    // ===================== A warps: gy^T (row = channel) -> TMEM hi / lo =====================
+    const int q = warp & 3, par = warp >= 8 ? 1 : 0;
+    const int cs = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    uint32_t it = 0;
+    for (Cur c = start_at(blockIdx.x); c.t < nitems; adv(c), ++it) {
+      if ((int)(it & 1) != par) continue;
+      const int s = it % W4_T, as = it % W4_AS;
+      mbar_wait(full + s, (it / W4_T) & 1);
+      const float* ga = reinterpret_cast<const float*>(smem + s * W4_TS);
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int px = 0; px < 32; ++px) {
+        const float v = ga[px * 64 + cs];  // a warp reads one 128-byte run per pixel row
+        hi[px] = __float_as_uint(v);
+        lo[px] = __float_as_uint(v - tf32_trunc(v));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tfree + s);
+      mbar_wait(afree + as, ((it / W4_AS) & 1) ^ 1);
+      tc_fence_after();
+      tmem_st32(tmem + lane_off + as * 64, hi);
+      if (X3) tmem_st32(tmem + lane_off + as * 64 + 32, lo);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(aready + as);
+    }
+  } else if (warp >= 6) {
+    // ===================== gather: B = im2col(x), K-major SW128 (+ lo) =====================
     // B is K-major (row n = tap * 4 + c holds the k-block's 32 pixels, 128 B,
     // 128-byte swizzle: 16-byte chunk j of row n at chunk j ^ (n % 8)); tcgen05
     // takes tf32 MN-major operands only in the 128B_BASE32B swizzle, which a
-    // 16-byte-per-tap gather cannot fill contiguously.  Loads run three
-    // k-blocks ahead of the stores (L2 latency >> one k-block of MMAs).
-    // four groups of two warps take every fourth k-block: a group's body is a
-    // dependency chain (barrier, loads, splits, stores, proxy fence, arrive), so
-    // k-blocks in flight, not warps per k-block, set the gather throughput
-    const int grp = (warp - 4) >> 1;
-    const int gt = (tid - 128) & 63;
-    // element i of this thread (8 per k-block): kernel row ki = 2 w + i / 4, pixel
+    // 16-byte-per-tap gather cannot fill contiguously
+    const int gi = warp < 8 ? warp - 6 : warp - 8;  // 0..7 over warps 6, 7, 10..15
+    const int grp = gi >> 1;
+    const int w2 = gi & 1, odd = lane & 1;
+    // element i of this thread (8 per k-block): kernel row ki = 2 w2 + i / 4, pixel
     // px = lane / 2 + 16 (i & 1), kernel column from the lane pair: (1, 2) for
     // i & 2 == 0, (0, 3) otherwise -- a warp's 32 loads then cover ~32 adjacent
     // input columns of one row (contiguous patch reads), and the two rows a
     // store instruction hits (taps kj, kj') sit four swizzle phases apart
-    const int w2 = gt >> 5, odd = lane & 1;
     auto elem = [&](int i, int& tap, int& px) {
       const int ki = 2 * w2 + (i >> 2);
       const int kj = (i & 2) ? (odd ? 3 : 0) : 1 + odd;
       tap = ki * 4 + kj;
       px = (lane >> 1) + 16 * (i & 1);
-    };
-    struct Cur {
-      int t, kb, nkb;
-    };
-    auto start_at = [&](int t) { return Cur{t, 0, t < nitems ? chunk_kblocks(P, t % P.nchunk) : 0}; };
-    auto adv = [&](Cur& c) {
-      if (++c.kb >= c.nkb) c = start_at(c.t + (int)gridDim.x);
     };
     uint32_t it = 0;
     for (Cur c = start_at(blockIdx.x); c.t < nitems; adv(c), ++it) {
@@ -194,16 +235,7 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
             cur[i] = __ldg(reinterpret_cast<const float4*>(x + (((long long)b * g.GH + iy) * g.GW + ix) * 4));
         }
       }
-      mbar_wait(full + s, (it / W4_T) & 1);          // A (+ patch) landed
-      mbar_wait(ofree + o, ((it / W4_O) & 1) ^ 1);  // operand slot free (its MMAs retired)
-      float* bh = reinterpret_cast<float*>(ops + o * W4_OS + W4_A + W4_B);
-      float* bl = reinterpret_cast<float*>(ops + o * W4_OS + W4_A);
-      const float4* ah = reinterpret_cast<const float4*>(smem + s * W4_TS);
-      float4 a4[W4_A / 16 / 64];
-      if (X3) {
-#pragma unroll
-        for (int i = 0; i < W4_A / 16 / 64; ++i) a4[i] = ah[gt + 64 * i];
-      }
+      mbar_wait(full + s, (it / W4_T) & 1);          // gy (+ patch) landed
       if (PATCH) {
         const float4* xp = reinterpret_cast<const float4*>(smem + s * W4_TS + W4_A);
 #pragma unroll
@@ -214,6 +246,11 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
           cur[i] = (pc >= 0 && pc < g.GW) ? xp[pr * g.GW + pc] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tfree + s);  // the slot is read (the A warps release their part)
+      mbar_wait(ofree + o, ((it / W4_O) & 1) ^ 1);  // operand slot free (its MMAs retired)
+      float* bl = reinterpret_cast<float*>(ops + o * W4_OS);
+      float* bh = reinterpret_cast<float*>(ops + o * W4_OS + W4_B);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float e4[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
@@ -227,26 +264,15 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
           if (X3) bl[off] = e4[c4] - tf32_trunc(e4[c4]);
         }
       }
-      if (X3) {
-        float4* al = reinterpret_cast<float4*>(ops + o * W4_OS);
-#pragma unroll
-        for (int i = 0; i < W4_A / 16 / 64; ++i) {
-          const float4 a = a4[i];
-          al[gt + 64 * i] =
-              make_float4(a.x - tf32_trunc(a.x), a.y - tf32_trunc(a.y), a.z - tf32_trunc(a.z), a.w - tf32_trunc(a.w));
-        }
-      }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(ready + o);
     }
   } else if (warp == 3) {
-    // ===================== MMA issue =====================
-    constexpr uint32_t idesc = make_idesc(128, 64, true, false);
-    const uint64_t a0 = make_desc(smem_u32(smem), 4096u, 512u, UMMA_SW128_BASE32B);
-    const uint64_t al0 = make_desc(smem_u32(ops), 4096u, 512u, UMMA_SW128_BASE32B);
-    const uint64_t bl0 = make_desc(smem_u32(ops) + W4_A, 16u, 1024u, UMMA_SW128);
-    const uint64_t b0 = make_desc(smem_u32(ops) + W4_A + W4_B, 16u, 1024u, UMMA_SW128);
+    // ===================== MMA issue (TS form: A = gy^T from TMEM) =====================
+    constexpr uint32_t idesc = make_idesc(128, 64, false, false);
+    const uint64_t bl0 = make_desc(smem_u32(ops), 16u, 1024u, UMMA_SW128);
+    const uint64_t b0 = make_desc(smem_u32(ops) + W4_B, 16u, 1024u, UMMA_SW128);
     uint32_t it = 0, sc = 0;
     for (int t = blockIdx.x; t < nitems; t += gridDim.x) {
       const int nkb = chunk_kblocks(P, t % P.nchunk);
@@ -254,28 +280,31 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
         const uint32_t buf = sc & 1;
         mbar_wait(seg_empty + buf, ((sc >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + buf * 64;
+        const uint32_t d0 = tmem + W4_ACOL + buf * (64 * W4_NACC);
         const int k_end = min(nkb, k_seg + W4_KSEG);
         for (int kb = k_seg; kb < k_end; ++kb, ++it) {
-          const int s = it % W4_T, o = it % W4_O;
-          mbar_wait(ready + o, (it / W4_O) & 1);  // the gather saw slot s land before it arrived
+          const int o = it % W4_O, as = it % W4_AS;
+          mbar_wait(ready + o, (it / W4_O) & 1);
+          mbar_wait(aready + as, (it / W4_AS) & 1);
           tc_fence_after();
-          const uint64_t so = (uint64_t)((s * W4_TS) >> 4), sl = (uint64_t)((o * W4_OS) >> 4);
+          const uint64_t sl = (uint64_t)((o * W4_OS) >> 4);
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < W4_KB / 8; ++kk) {
-              const uint64_t ah = a0 + so + (kk * 1024 >> 4), bh = b0 + sl + (kk * 32 >> 4);
-              const uint32_t acc = (kb != k_seg || kk) ? 1u : 0u;
+              const uint32_t a_t = tmem + as * 64 + kk * 8;
+              const uint64_t bh = b0 + sl + (kk * 32 >> 4);
+              const uint32_t d = d0 + (kk % W4_NACC) * 64;
+              const uint32_t acc = (kb != k_seg || kk >= W4_NACC) ? 1u : 0u;
               if (X3) {
-                mma_tf32(d, al0 + sl + (kk * 1024 >> 4), bh, idesc, acc);  // small terms first
-                mma_tf32(d, ah, bl0 + sl + (kk * 32 >> 4), idesc, 1u);
-                mma_tf32(d, ah, bh, idesc, 1u);
+                mma_tf32_ts_w4(d, a_t + 32, bh, idesc, acc);  // small terms first
+                mma_tf32_ts_w4(d, a_t, bl0 + sl + (kk * 32 >> 4), idesc, 1u);
+                mma_tf32_ts_w4(d, a_t, bh, idesc, 1u);
               } else {
-                mma_tf32(d, ah, bh, idesc, acc);
+                mma_tf32_ts_w4(d, a_t, bh, idesc, acc);
               }
             }
-            mma_commit(tfree + s);
             mma_commit(ofree + o);
+            mma_commit(afree + as);
             if (kb + 1 == k_end) mma_commit(seg_full + buf);
           }
           __syncwarp();
@@ -298,13 +327,15 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
         mbar_wait(seg_full + buf, (sc >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tmem + lane_base + buf * 64 + c * 32, r);
-          tmem_ld_wait();
+        for (int a = 0; a < W4_NACC; ++a)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc[c * 32 + i] += __uint_as_float(r[i]);
-        }
+          for (int c = 0; c < 2; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tmem + lane_base + W4_ACOL + buf * (64 * W4_NACC) + a * 64 + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[c * 32 + i] += __uint_as_float(r[i]);
+          }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(seg_empty + buf);
@@ -318,7 +349,7 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
   __syncthreads();
   if (warp == 3) {
     tc_fence_after();
-    tmem_dealloc(tmem, 128);
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -353,9 +384,9 @@ cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, 
   CUtensorMap tm;
   const long long dims[3] = {g.CS, P.K, a.L};
   const long long strides[2] = {g.CS, a.small_ls};
-  const int box[3] = {32, W4_KB, 1};
+  const int box[3] = {64, W4_KB, 1};
   const int one[3] = {1, 1, 1};
-  if (!make_map(&tm, a.small, 3, dims, strides, box, one, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+  if (!make_map(&tm, a.small, 3, dims, strides, box, one, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   // patch mode: a k-block = 32 / SW whole output rows of one image, whose input
   // rows (GW * 4 floats each) arrive as one TMA box next to the gy boxes
