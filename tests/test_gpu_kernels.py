@@ -423,3 +423,79 @@ def test_caller_owned_workspace(native, torch_cuda):
         assert needs[N.PG_OP_CONV2D_BWD_FILTER] > 0, needs
     finally:
         native.pg_set_workspace(None, None, 0)
+
+
+@pytest.mark.parametrize("math,tol", [(1, 1e-5), (2, 5e-3)])
+def test_image_side_many_labels_per_cta(native, torch_cuda, math, tol):
+    """The 4-channel image-side kernels (fprop4 / dgrad4 / wgrad4) walk a
+    contiguous tile range per CTA and rebuild the label's weights on a label
+    change; with 300 labels of one image each, every CTA crosses 2-3 labels.
+    Checked per label against float64 torch (grouped conv = one label per
+    group), including the generator's bias + tanh convT4 epilogue."""
+    torch = torch_cuda
+    import torch.nn.functional as F
+    from paper_2102_10485_b200 import _native as N
+    L, B, H = 300, 1, 64
+    g = torch.Generator().manual_seed(11)
+    x = torch.randn(L, B, 3, H, H, generator=g, dtype=torch.float64)
+    w = 0.2 * torch.randn(L, 64, 3, 4, 4, generator=g, dtype=torch.float64)  # conv1: [Cout][Cin][k][k]
+    b = 0.1 * torch.randn(L, 64, generator=g, dtype=torch.float64)
+    gy = torch.randn(L, B, 64, H // 2, H // 2, generator=g, dtype=torch.float64)
+    wt = 0.2 * torch.randn(L, 64, 3, 4, 4, generator=g, dtype=torch.float64)  # convT4: [Cin][Cout][k][k]
+    bt = 0.1 * torch.randn(L, 3, generator=g, dtype=torch.float64)
+    # float64 references, labels as groups
+    xg = x.permute(1, 0, 2, 3, 4).reshape(B, L * 3, H, H)
+    y_ref = F.conv2d(xg, w.reshape(L * 64, 3, 4, 4), b.reshape(-1), stride=2, padding=1, groups=L)
+    gyg = gy.permute(1, 0, 2, 3, 4).reshape(B, L * 64, H // 2, H // 2)
+    gx_ref = F.conv_transpose2d(gyg, w.reshape(L * 64, 3, 4, 4), stride=2, padding=1, groups=L)
+    gw_ref = torch.stack([torch.nn.grad.conv2d_weight(x[l], w[l].shape, gy[l], stride=2, padding=1) for l in range(L)])
+    pre_ref = F.conv_transpose2d(gyg, wt.reshape(L * 64, 3, 4, 4), bt.reshape(-1), stride=2, padding=1, groups=L)
+    yt_ref = torch.tanh(pre_ref)
+
+    def nhwc4(t):  # [L][B][C][h][w] -> [L][B][h][w][4] fp32 on the device
+        out = torch.zeros(*t.shape[:2], t.shape[3], t.shape[4], 4, dtype=torch.float32)
+        out[..., :t.shape[2]] = t.permute(0, 1, 3, 4, 2).float()
+        return out.cuda()
+
+    x_d = nhwc4(x)
+    gy_d = gy.permute(0, 1, 3, 4, 2).float().contiguous().cuda()
+    w_d = torch.zeros(L, 64, 16, 4)
+    w_d[..., :3] = w.permute(0, 1, 3, 4, 2).reshape(L, 64, 16, 3).float()
+    w_d = w_d.reshape(L, -1).cuda()
+    wt_d = torch.zeros(L, 64, 16, 4)
+    wt_d[..., :3] = wt.permute(0, 1, 3, 4, 2).reshape(L, 64, 16, 3).float()
+    wt_d = wt_d.reshape(L, -1).cuda()
+    b_d = b.float().cuda()
+    bt_d = torch.zeros(L, 4)
+    bt_d[:, :3] = bt.float()
+    bt_d = bt_d.cuda()
+    d = N.ConvDesc(B=B, Cin=3, H=H, W=H, Cout=64, OH=H // 2, OW=H // 2, k=4, s=2, p=1)
+    dT = N.ConvDesc(B=B, Cin=64, H=H // 2, W=H // 2, Cout=3, OH=H, OW=H, k=4, s=2, p=1)
+    y_d = torch.zeros(L, B, H // 2, H // 2, 64, device="cuda")
+    gx_d = torch.zeros(L, B, H, H, 4, device="cuda")
+    gw_d = torch.zeros_like(w_d)
+    yt_d = torch.zeros(L, B, H, H, 4, device="cuda")
+    N.check(native.pg_conv2d_fwd(C.byref(d), L, ptr(x_d), ptr(w_d), w_d.shape[1], ptr(b_d), 64, 0, 0.0, ptr(y_d),
+                                 math, None), "fwd")
+    N.check(native.pg_conv2d_bwd_data(C.byref(d), L, ptr(gy_d), ptr(w_d), w_d.shape[1], ptr(gx_d), math, None), "dgrad")
+    N.check(native.pg_conv2d_bwd_filter(C.byref(d), L, ptr(x_d), ptr(gy_d), ptr(gw_d), w_d.shape[1], 0, math, None),
+            "wgrad")
+    N.check(native.pg_convT2d_fwd(C.byref(dT), L, ptr(gy_d), ptr(wt_d), wt_d.shape[1], ptr(bt_d), 4, N.ACT_TANH, 0.0,
+                                  ptr(yt_d), math, None), "convT fwd")
+    torch.cuda.synchronize()
+    y = y_d.cpu().double().permute(0, 1, 4, 2, 3)  # [L][B][64][h][w]
+    gx = gx_d.cpu().double()[..., :3].permute(0, 1, 4, 2, 3)
+    gw = gw_d.cpu().double().reshape(L, 64, 4, 4, 4)[..., :3].permute(0, 1, 4, 2, 3)
+    yt = yt_d.cpu().double()[..., :3].permute(0, 1, 4, 2, 3)
+    y_ref = y_ref.reshape(B, L, 64, H // 2, H // 2).permute(1, 0, 2, 3, 4)
+    gx_ref = gx_ref.reshape(B, L, 3, H, H).permute(1, 0, 2, 3, 4)
+    yt_ref = yt_ref.reshape(B, L, 3, H, H).permute(1, 0, 2, 3, 4)
+    pre_ref = pre_ref.reshape(B, L, 3, H, H).permute(1, 0, 2, 3, 4)
+    worst = {}
+    # tanh is 1-Lipschitz: its error is held to the tolerance of the pre-activation it saturates
+    for name, got, ref, scale in (("fwd", y, y_ref, y_ref), ("dgrad", gx, gx_ref, gx_ref), ("wgrad", gw, gw_ref, gw_ref),
+                                  ("convT", yt, yt_ref, pre_ref)):
+        err = ((got - ref).abs().amax(dim=(1, 2, 3, 4)) / scale.abs().amax(dim=(1, 2, 3, 4))).max()
+        worst[name] = float(err)
+    assert max(worst.values()) < tol, worst
+    assert torch.all(gx_d[..., 3] == 0) and torch.all(yt_d[..., 3] == 0)
