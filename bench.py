@@ -28,7 +28,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-MATH = {"fp32": 0, "tf32x3": 1, "tf32": 2}
+MATH = {"fp32": 0, "tf32x3": 1, "tf32": 2, "bf16": 3}
 
 
 def parse():
@@ -350,7 +350,8 @@ def main():
             "metric": "GAN train images/sec (G+D step, whole box)", "value": value, "unit": "images/s",
             "n_gpus": world, "steps": ran, "warmup": args.warmup, "ms_per_step": max_ms / max(ran, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": {"fp32": "fp32", "tf32x3": "fp32 (3xTF32 split on tcgen05)", "tf32": "tf32"}[args.math],
+            "dtype": {"fp32": "fp32", "tf32x3": "fp32 (3xTF32 split on tcgen05)", "tf32": "tf32",
+                      "bf16": "bf16 GEMM operands, fp32 accumulation"}[args.math],
             "data": "synthetic (per-label cosine fields + N(0,0.1^2) noise, 1280/label)",
             "config": {"workload": f"c{args.cfg} arch sweep: {Lg} labels/GPU, per-label batch {args.batch}, "
                                    f"{'x'.join(map(str, arch.image))}", "labels_per_gpu": Lg,

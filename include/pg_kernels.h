@@ -30,8 +30,13 @@ enum { PG_OK = 0, PG_EINVAL = -1, PG_ECUDA = -2, PG_ENONFINITE = -3, PG_EUNSUPPO
 
 /* Math modes for the GEMM-shaped kernels.  FP32_SIMT: exact fp32 FMAs on the
  * CUDA cores.  TF32X3: tcgen05 kind::tf32 with the 3-pass split
- * (a_hi*b_hi + a_hi*b_lo + a_lo*b_hi), fp32-accurate.  TF32: one tcgen05 pass. */
-enum { PG_MATH_FP32_SIMT = 0, PG_MATH_TF32X3 = 1, PG_MATH_TF32 = 2 };
+ * (a_hi*b_hi + a_hi*b_lo + a_lo*b_hi), fp32-accurate.  TF32: one tcgen05 pass.
+ * BF16: the tensor-core GEMMs round both operands to bfloat16 (nearest even)
+ * and multiply them in one kind::tf32 pass with fp32 accumulation -- a bf16 x
+ * bf16 -> fp32 product (bf16 values are exact in tf32, their products exact in
+ * fp32); operands stay fp32 in memory, so it runs at the TF32 rate.  The SIMT
+ * dense-head kernels compute in fp32 in every mode. */
+enum { PG_MATH_FP32_SIMT = 0, PG_MATH_TF32X3 = 1, PG_MATH_TF32 = 2, PG_MATH_BF16 = 3 };
 
 /* Activations fused into epilogues (network.cpp:384-391). */
 enum { PG_ACT_NONE = 0, PG_ACT_RELU = 1, PG_ACT_LRELU = 2, PG_ACT_TANH = 3, PG_ACT_SIGMOID = 4 };

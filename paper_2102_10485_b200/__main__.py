@@ -33,7 +33,7 @@ from .archs import baseline_arch, with_bn
 from .runconfig import ConfigError, load_config_file
 from .trainer import AdamConfig, GroupSpec, LabelGroup, derive_seed, estimate_priors
 
-MATH = {"fp32": N.MATH_FP32_SIMT, "tf32x3": N.MATH_TF32X3, "tf32": N.MATH_TF32}
+MATH = {"fp32": N.MATH_FP32_SIMT, "tf32x3": N.MATH_TF32X3, "tf32": N.MATH_TF32, "bf16": N.MATH_BF16}
 
 
 def _rank_world() -> tuple[int, int, int]:

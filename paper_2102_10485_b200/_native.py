@@ -14,7 +14,7 @@ LIB_PATH = Path(os.environ.get("PG_LIB", "")) if os.environ.get("PG_LIB") else \
     Path(__file__).resolve().parent / "_lib" / "libpartgan_b200.so"  # PG_LIB: tuning-variant builds only
 
 PG_OK, PG_EINVAL, PG_ECUDA, PG_ENONFINITE, PG_EUNSUPPORTED = 0, -1, -2, -3, -4
-MATH_FP32_SIMT, MATH_TF32X3, MATH_TF32 = 0, 1, 2
+MATH_FP32_SIMT, MATH_TF32X3, MATH_TF32, MATH_BF16 = 0, 1, 2, 3
 ACT_NONE, ACT_RELU, ACT_LRELU, ACT_TANH, ACT_SIGMOID = 0, 1, 2, 3, 4
 (PG_OP_CONV2D_FWD, PG_OP_CONV2D_BWD_DATA, PG_OP_CONV2D_BWD_FILTER, PG_OP_CONVT2D_FWD, PG_OP_CONVT2D_BWD_DATA,
  PG_OP_CONVT2D_BWD_FILTER, PG_OP_DENSE_FWD, PG_OP_DENSE_BWD_DATA, PG_OP_DENSE_BWD_FILTER) = range(9)

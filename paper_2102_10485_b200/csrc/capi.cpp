@@ -206,6 +206,7 @@ pg::GemmArgs op_args(int op, const pg_conv_desc* d, int L, const OpPtrs& p) {
 
 int run_op(int op, const pg_conv_desc* d, int L, const OpPtrs& p, int math, void* stream, const char* what) {
   return guard([&] {
+    if (math < PG_MATH_FP32_SIMT || math > PG_MATH_BF16) throw std::invalid_argument("unknown math mode");
     const pg::GemmArgs a = op_args(op, d, L, p);
     cuda_ok(pg::launch_gemm(a, math, S(stream)), what);
   });
@@ -288,7 +289,7 @@ int pg_dense_bwd_filter(int L, int B, int in, int out, const float* x, const flo
 size_t pg_workspace_size(int op, const pg_conv_desc* d, int L, int math) {
   size_t bytes = 0;
   const int rc = guard([&] {
-    if (math < PG_MATH_FP32_SIMT || math > PG_MATH_TF32) throw std::invalid_argument("unknown math mode");
+    if (math < PG_MATH_FP32_SIMT || math > PG_MATH_BF16) throw std::invalid_argument("unknown math mode");
     OpPtrs p;  // null device pointers pass every alignment test; strides as the arenas would have them
     const pg::GemmArgs probe = op_args(op, d, L, p);
     const pg::ConvGeo& g = probe.g;
@@ -415,6 +416,7 @@ int pg_group_create(const pg_group_config* c, pg_group** out) {
     cfg.eps = c->eps;
     cfg.clamp = c->clamp;
     cfg.init_std = c->init_std;
+    if (c->math < PG_MATH_FP32_SIMT || c->math > PG_MATH_BF16) throw std::invalid_argument("unknown math mode");
     cfg.math = c->math;
     cfg.threads = c->threads;
     if (c->seeds) cfg.seeds.assign(c->seeds, c->seeds + c->n_labels);

@@ -128,9 +128,10 @@ PG_DEV void d4_tile(const D4Plan& P, int t, int& label, int& b, int& p0, int& ib
   ib0 = p0 / P.gw1;
 }
 
-template <bool X3>
+template <int MODE>
 __global__ void __launch_bounds__(D4_NT, 1)
     dgrad4_kernel(const __grid_constant__ CUtensorMap tmS, const D4Plan P) {
+  constexpr bool X3 = MODE == MATH_TF32X3, RND = MODE == MATH_BF16;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* bhi = smem + D4_PS * D4_PATCH;  // [D4_WB][D4_B]
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(D4_NT, 1)
           const int ki = (ph >> 1) + 2 * (nbr >> 1), kj = (ph & 1) + 2 * (nbr & 1);
           const float v = c < g.CG ? __ldg(w + ((long long)cs * 16 + ki * 4 + kj) * g.CG + c) : 0.f;
           const int off = (k >> 5) * 2048 + n * 128 + ((((k & 31) >> 2) ^ (n & 7)) << 4) + (k & 3) * 4;
-          *reinterpret_cast<float*>(bhi + wb * D4_B + off) = v;
+          *reinterpret_cast<float*>(bhi + wb * D4_B + off) = RND ? bf16_rne(v) : v;
           *reinterpret_cast<float*>(blo + wb * D4_B + off) = v - tf32_trunc(v);
         }
         fence_async_smem();
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(D4_NT, 1)
           const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int uu = 0; uu < 4; ++uu) {
-            hi[4 * c + uu] = __float_as_uint(e[uu]);
+            hi[4 * c + uu] = __float_as_uint(RND ? bf16_rne(e[uu]) : e[uu]);
             lo[4 * c + uu] = __float_as_uint(e[uu] - tf32_trunc(e[uu]));
           }
         }
@@ -404,7 +405,7 @@ cudaError_t launch_dgrad4(const GemmArgs& a, int math, cudaStream_t st) {
   if (!make_map(&ts, a.small, 5, sd, ss, sb, one, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   static PerDeviceOnce configured;
   cudaError_t e = configured.run([] {
-    for (auto f : {dgrad4_kernel<true>, dgrad4_kernel<false>}) {
+    for (auto f : {dgrad4_kernel<MATH_TF32X3>, dgrad4_kernel<MATH_TF32>, dgrad4_kernel<MATH_BF16>}) {
       cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, D4_SMEM);
       if (r != cudaSuccess) return r;
     }
@@ -415,9 +416,11 @@ cudaError_t launch_dgrad4(const GemmArgs& a, int math, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
   const int grid = std::min(ntiles, sm_count_tma());
   if (math == MATH_TF32X3)
-    dgrad4_kernel<true><<<grid, D4_NT, D4_SMEM, st>>>(ts, P);
+    dgrad4_kernel<MATH_TF32X3><<<grid, D4_NT, D4_SMEM, st>>>(ts, P);
+  else if (math == MATH_BF16)
+    dgrad4_kernel<MATH_BF16><<<grid, D4_NT, D4_SMEM, st>>>(ts, P);
   else
-    dgrad4_kernel<false><<<grid, D4_NT, D4_SMEM, st>>>(ts, P);
+    dgrad4_kernel<MATH_TF32><<<grid, D4_NT, D4_SMEM, st>>>(ts, P);
   return launched();
 }
 

@@ -102,10 +102,11 @@ PG_DEV void f4_stage(float (&acc)[32], const float (&b)[32], const F4Plan& P, in
         make_float4(acc[4 * c4], acc[4 * c4 + 1], acc[4 * c4 + 2], acc[4 * c4 + 3]);
 }
 
-template <bool X3>
+template <int MODE>
 __global__ void __launch_bounds__(F4_NT, 1)
     fprop4_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                   const __grid_constant__ CUtensorMap tmO, const F4Plan P) {
+  constexpr bool X3 = MODE == MATH_TF32X3, RND = MODE == MATH_BF16;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* whi = smem + F4_PS * F4_PATCH;  // [2][F4_W]
@@ -199,6 +200,10 @@ __global__ void __launch_bounds__(F4_NT, 1)
                                  v.w - tf32_trunc(v.w));
           }
           fence_async_smem();
+        } else if (RND) {  // bf16 operands: round the landed weights in place
+          float4* v4 = reinterpret_cast<float4*>(whi + wb * F4_W);
+          for (int e = gw * 32 + lane; e < F4_W / 16; e += 128) v4[e] = bf16_rne4(v4[e]);
+          fence_async_smem();
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(wready + wb);
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(F4_NT, 1)
         const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          hi[4 * tt + u] = __float_as_uint(e[u]);
+          hi[4 * tt + u] = __float_as_uint(RND ? bf16_rne(e[u]) : e[u]);
           lo[4 * tt + u] = __float_as_uint(e[u] - tf32_trunc(e[u]));
         }
       }
@@ -393,7 +398,7 @@ cudaError_t launch_fprop4(const GemmArgs& a, int math, cudaStream_t st) {
   if (!make_map(&to, a.out, 3, od, os, ob, one, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   static PerDeviceOnce configured;
   cudaError_t e = configured.run([] {
-    for (auto f : {fprop4_kernel<true>, fprop4_kernel<false>}) {
+    for (auto f : {fprop4_kernel<MATH_TF32X3>, fprop4_kernel<MATH_TF32>, fprop4_kernel<MATH_BF16>}) {
       cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, F4_SMEM);
       if (r != cudaSuccess) return r;
     }
@@ -404,13 +409,15 @@ cudaError_t launch_fprop4(const GemmArgs& a, int math, cudaStream_t st) {
   const int grid = std::min(ntiles, sm_count_tma());
   if (ntiles == 0) return cudaSuccess;
   if (math == MATH_TF32X3)
-    fprop4_kernel<true><<<grid, F4_NT, F4_SMEM, st>>>(tx, tw, to, P);
+    fprop4_kernel<MATH_TF32X3><<<grid, F4_NT, F4_SMEM, st>>>(tx, tw, to, P);
+  else if (math == MATH_BF16)
+    fprop4_kernel<MATH_BF16><<<grid, F4_NT, F4_SMEM, st>>>(tx, tw, to, P);
   else
-    fprop4_kernel<false><<<grid, F4_NT, F4_SMEM, st>>>(tx, tw, to, P);
+    fprop4_kernel<MATH_TF32><<<grid, F4_NT, F4_SMEM, st>>>(tx, tw, to, P);
   const cudaError_t le = launched();
   if (le != cudaSuccess && std::getenv("PG_F4_DIAG")) {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, fprop4_kernel<true>);
+    cudaFuncGetAttributes(&fa, fprop4_kernel<MATH_TF32X3>);
     fprintf(stderr, "fprop4 launch: %s regs=%d maxthreads=%d smem_static=%zu maxdyn=%d local=%zu want dyn=%d threads=%d\n",
             cudaGetErrorString(le), fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes,
             fa.localSizeBytes, F4_SMEM, F4_NT);

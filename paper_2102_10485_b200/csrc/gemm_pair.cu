@@ -657,6 +657,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_nt(KIND, BN, MO
                                  v.w - tf32_trunc(v.w));
           }
           fence_async_smem();
+        } else if (MODE == MATH_BF16) {
+          // bf16 operands: round the landed A rows and B half in place
+          float4* v4 = reinterpret_cast<float4*>(smem + s * SB);
+#pragma unroll 8
+          for (int i = st; i < SB / 16; i += NSPLIT * 32) v4[i] = bf16_rne4(v4[i]);
+          fence_async_smem();
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(ready_leader + r * 8);
@@ -1339,24 +1345,21 @@ cudaError_t launch_gemm_pair(const GemmArgs& a, int math, cudaStream_t st) {
     P.stat = buf;
   }
   if (P.stat_mode != STAT_NONE && (!P.stat || P.N % 8 || P.act != ACT_NONE)) return cudaErrorInvalidValue;
-  const bool x3 = math != MATH_TF32;
-  if (dgrad_packed(a))
-    return x3 ? launch_pair_kind<KIND_DGP, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
-              : launch_pair_kind<KIND_DGP, MATH_TF32>(ta, tb, tbl, P, bn, st);
-  if (f4)
-    return x3 ? launch_pair_kind<KIND_F4, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
-              : launch_pair_kind<KIND_F4, MATH_TF32>(ta, tb, tbl, P, bn, st);
-  switch (a.kind) {
-    case GEMM_FPROP:
-      return x3 ? launch_pair_kind<GEMM_FPROP, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
-                : launch_pair_kind<GEMM_FPROP, MATH_TF32>(ta, tb, tbl, P, bn, st);
-    case GEMM_DGRAD:
-      return x3 ? launch_pair_kind<GEMM_DGRAD, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
-                : launch_pair_kind<GEMM_DGRAD, MATH_TF32>(ta, tb, tbl, P, bn, st);
-    default:
-      return x3 ? launch_pair_kind<GEMM_WGRAD, MATH_TF32X3>(ta, tb, tbl, P, bn, st)
-                : launch_pair_kind<GEMM_WGRAD, MATH_TF32>(ta, tb, tbl, P, bn, st);
+  // one instantiation per math mode (TF32X3 three-pass split, TF32 one pass, BF16 one pass on rounded operands)
+#define PG_PAIR_MODES(K)                                                            \
+  switch (math) {                                                                   \
+    case MATH_TF32: return launch_pair_kind<K, MATH_TF32>(ta, tb, tbl, P, bn, st);  \
+    case MATH_BF16: return launch_pair_kind<K, MATH_BF16>(ta, tb, tbl, P, bn, st);  \
+    default: return launch_pair_kind<K, MATH_TF32X3>(ta, tb, tbl, P, bn, st);       \
   }
+  if (dgrad_packed(a)) PG_PAIR_MODES(KIND_DGP)
+  if (f4) PG_PAIR_MODES(KIND_F4)
+  switch (a.kind) {
+    case GEMM_FPROP: PG_PAIR_MODES(GEMM_FPROP)
+    case GEMM_DGRAD: PG_PAIR_MODES(GEMM_DGRAD)
+    default: PG_PAIR_MODES(GEMM_WGRAD)
+  }
+#undef PG_PAIR_MODES
 }
 
 }  // namespace pg

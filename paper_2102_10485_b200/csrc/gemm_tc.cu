@@ -344,6 +344,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(GemmArgs a, TileGr
         for (int it = 0; it < NB; ++it)
           if (b_off[it] >= 0) store_lo(b_lo + b_off[it], vb[it]);
       }
+      if (MODE == MATH_BF16) {  // bf16 operands: round this thread's chunks in place
+        uint8_t* a_hi = smem + s * STAGE;
+        uint8_t* b_hi = a_hi + A_BYTES;
+#pragma unroll
+        for (int c = 0; c < NA; ++c) {
+          float4* p = reinterpret_cast<float4*>(a_hi + a_off[c]);
+          *p = bf16_rne4(*p);
+        }
+#pragma unroll
+        for (int it = 0; it < NB; ++it)
+          if (b_off[it] >= 0) {
+            float4* p = reinterpret_cast<float4*>(b_hi + b_off[it]);
+            *p = bf16_rne4(*p);
+          }
+      }
       fence_async_smem();
       mbar_arrive(full + s);
       ++done;
@@ -550,6 +565,7 @@ cudaError_t launch_gemm_tc(const GemmArgs& a, int math, cudaStream_t st) {
     return cudaMemcpyToSymbol(c_dbg, &v, sizeof(int));
   });
   if (math == MATH_TF32) return launch_mode<MATH_TF32>(a, st);
+  if (math == MATH_BF16) return launch_mode<MATH_BF16>(a, st);
   return launch_mode<MATH_TF32X3>(a, st);
 }
 

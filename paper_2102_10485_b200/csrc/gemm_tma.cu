@@ -94,7 +94,9 @@ template <int KIND, int BN, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const TmaPlan P) {
-  constexpr bool SPLIT = MODE == MATH_TF32X3;
+  // BF16 runs the three-pass pipeline with hi rounded in place and lo = 0 (this
+  // engine only takes the shapes the pair engine does not)
+  constexpr bool SPLIT = MODE == MATH_TF32X3 || MODE == MATH_BF16;
   constexpr int SH = hi_stages(BN, SPLIT);
   constexpr int SL = lo_stages(BN, SPLIT);
   constexpr int HI = hi_bytes(BN);
@@ -209,8 +211,13 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll 4
           for (int i = st; i < HI / 16; i += 128) {
             const float4 v = src[i];
-            dst[i] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
-                                 v.w - tf32_trunc(v.w));
+            if (MODE == MATH_BF16) {
+              const_cast<float4*>(src)[i] = bf16_rne4(v);
+              dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+              dst[i] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                                   v.w - tf32_trunc(v.w));
+            }
           }
           fence_async_smem();
           mbar_arrive(full_l + j);
@@ -362,7 +369,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 template <int KIND, int BN, int MODE>
 cudaError_t launch_tma_bn(const CUtensorMap& ta, const CUtensorMap& tb, const TmaPlan& P, cudaStream_t st) {
-  constexpr int smem = smem_total(BN, MODE == MATH_TF32X3);
+  constexpr int smem = smem_total(BN, MODE == MATH_TF32X3 || MODE == MATH_BF16);
   static PerDeviceOnce configured;
   cudaError_t ce = configured.run([&] {
     return cudaFuncSetAttribute(gemm_tma_kernel<KIND, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -481,18 +488,18 @@ cudaError_t launch_gemm_tma(const GemmArgs& a, int math, cudaStream_t st) {
   }
   if (!ok) return cudaErrorInvalidValue;
   P.ntn = (P.N + bn - 1) / bn;
-  const bool x3 = math != MATH_TF32;
-  switch (a.kind) {
-    case GEMM_FPROP:
-      return x3 ? launch_tma_kind<GEMM_FPROP, MATH_TF32X3>(ta, tb, P, bn, st)
-                : launch_tma_kind<GEMM_FPROP, MATH_TF32>(ta, tb, P, bn, st);
-    case GEMM_DGRAD:
-      return x3 ? launch_tma_kind<GEMM_DGRAD, MATH_TF32X3>(ta, tb, P, bn, st)
-                : launch_tma_kind<GEMM_DGRAD, MATH_TF32>(ta, tb, P, bn, st);
-    default:
-      return x3 ? launch_tma_kind<GEMM_WGRAD, MATH_TF32X3>(ta, tb, P, bn, st)
-                : launch_tma_kind<GEMM_WGRAD, MATH_TF32>(ta, tb, P, bn, st);
+#define PG_TMA_MODES(K)                                                         \
+  switch (math) {                                                               \
+    case MATH_TF32: return launch_tma_kind<K, MATH_TF32>(ta, tb, P, bn, st);    \
+    case MATH_BF16: return launch_tma_kind<K, MATH_BF16>(ta, tb, P, bn, st);    \
+    default: return launch_tma_kind<K, MATH_TF32X3>(ta, tb, P, bn, st);         \
   }
+  switch (a.kind) {
+    case GEMM_FPROP: PG_TMA_MODES(GEMM_FPROP)
+    case GEMM_DGRAD: PG_TMA_MODES(GEMM_DGRAD)
+    default: PG_TMA_MODES(GEMM_WGRAD)
+  }
+#undef PG_TMA_MODES
 }
 
 }  // namespace pg

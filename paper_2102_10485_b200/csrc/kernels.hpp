@@ -6,7 +6,9 @@
 
 namespace pg {
 
-enum MathMode : int { MATH_FP32_SIMT = 0, MATH_TF32X3 = 1, MATH_TF32 = 2 };
+// MATH_BF16: tensor-core GEMM operands rounded to bfloat16 (nearest even),
+// one kind::tf32 MMA pass, fp32 accumulation; the SIMT kernels stay fp32
+enum MathMode : int { MATH_FP32_SIMT = 0, MATH_TF32X3 = 1, MATH_TF32 = 2, MATH_BF16 = 3 };
 
 // every launcher ends with `return launched();`: counts the kernel launch
 // (bench.py's gpu_launches) and returns the launch status

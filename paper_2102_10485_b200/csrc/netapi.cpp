@@ -96,6 +96,7 @@ int pg_net_create(const char* spec, const long* in_shape, int in_rank, uint64_t 
     *out = nullptr;
     auto n = std::make_unique<pg_net>();
     n->device = device;
+    if (math < PG_MATH_FP32_SIMT || math > PG_MATH_BF16) throw std::invalid_argument("unknown math mode");
     n->math = math;
     n->spec = spec;
     n->in_shape.assign(in_shape, in_shape + in_rank);

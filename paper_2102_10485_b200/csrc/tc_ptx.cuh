@@ -9,6 +9,16 @@
 
 namespace pg {
 
+// PG_MATH_BF16 operand rounding: nearest-even to bfloat16 (8-bit significand),
+// kept in an fp32 container; inf / NaN pass through.  bf16 values are exact in
+// tf32 and their products exact in fp32, so a kind::tf32 MMA on rounded
+// operands is a bf16 x bf16 -> fp32 product.
+PG_DEV float bf16_rne(float x) {
+  const uint32_t u = __float_as_uint(x);
+  if ((u & 0x7F800000u) == 0x7F800000u) return x;
+  return __uint_as_float((u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u);
+}
+PG_DEV float4 bf16_rne4(float4 v) { return make_float4(bf16_rne(v.x), bf16_rne(v.y), bf16_rne(v.z), bf16_rne(v.w)); }
 PG_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 PG_DEV void mbar_init(uint64_t* bar, uint32_t count) {

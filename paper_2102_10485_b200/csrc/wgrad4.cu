@@ -91,9 +91,10 @@ PG_DEV void mma_tf32_ts_w4(uint32_t tmem_d, uint32_t a_tmem, uint64_t bdesc, uin
 // channels 0..63), 2 TMA, 3 TMEM allocation + MMA issue, 4-5 and 8-9 A warps
 // (quarters 0, 1; even / odd k-blocks), 6-7 and 10-15 gather (four groups of
 // two warps, k-block it % 4 each).
-template <bool X3, bool PATCH>
+template <int MODE, bool PATCH>
 __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmX, const W4Plan P) {
+  constexpr bool X3 = MODE == MATH_TF32X3, RND = MODE == MATH_BF16;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ops = smem + W4_T * W4_TS;
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
 #pragma unroll
       for (int px = 0; px < 32; ++px) {
         const float v = ga[px * 64 + cs];  // a warp reads one 128-byte run per pixel row
-        hi[px] = __float_as_uint(v);
+        hi[px] = __float_as_uint(RND ? bf16_rne(v) : v);
         lo[px] = __float_as_uint(v - tf32_trunc(v));
       }
       __syncwarp();
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
         for (int c4 = 0; c4 < 4; ++c4) {
           const int n = tap * 4 + c4;
           const int off = n * 32 + (((px >> 2) ^ (n & 7)) << 2) + (px & 3);
-          bh[off] = e4[c4];
+          bh[off] = RND ? bf16_rne(e4[c4]) : e4[c4];
           if (X3) bl[off] = e4[c4] - tf32_trunc(e4[c4]);
         }
       }
@@ -404,8 +405,8 @@ cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, 
   }
   static PerDeviceOnce configured;
   cudaError_t e = configured.run([] {
-    for (auto f : {wgrad4_kernel<true, true>, wgrad4_kernel<true, false>, wgrad4_kernel<false, true>,
-                   wgrad4_kernel<false, false>}) {
+    for (auto f : {wgrad4_kernel<MATH_TF32X3, true>, wgrad4_kernel<MATH_TF32X3, false>, wgrad4_kernel<MATH_TF32, true>,
+                   wgrad4_kernel<MATH_TF32, false>, wgrad4_kernel<MATH_BF16, true>, wgrad4_kernel<MATH_BF16, false>}) {
       cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, W4_SMEM);
       if (r != cudaSuccess) return r;
     }
@@ -414,11 +415,13 @@ cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, 
   if (e != cudaSuccess) return e;
   const int items = a.L * nchunk;
   const int grid = std::min(items, sm_count_tma());
-  const bool x3 = math == MATH_TF32X3;
-  if (x3 && patch) wgrad4_kernel<true, true><<<grid, W4_NT, W4_SMEM, st>>>(tm, tx, P);
-  else if (x3) wgrad4_kernel<true, false><<<grid, W4_NT, W4_SMEM, st>>>(tm, tx, P);
-  else if (patch) wgrad4_kernel<false, true><<<grid, W4_NT, W4_SMEM, st>>>(tm, tx, P);
-  else wgrad4_kernel<false, false><<<grid, W4_NT, W4_SMEM, st>>>(tm, tx, P);
+#define PG_W4(M)                                                            \
+  (patch ? wgrad4_kernel<M, true><<<grid, W4_NT, W4_SMEM, st>>>(tm, tx, P)  \
+         : wgrad4_kernel<M, false><<<grid, W4_NT, W4_SMEM, st>>>(tm, tx, P))
+  if (math == MATH_TF32X3) PG_W4(MATH_TF32X3);
+  else if (math == MATH_BF16) PG_W4(MATH_BF16);
+  else PG_W4(MATH_TF32);
+#undef PG_W4
   return launched();
 }
 

@@ -1,7 +1,10 @@
 """Kernel-level parity through the C-ABI (include/pg_kernels.h) against the
 CPU oracle on identical seeded inputs, batched over several labels with
 distinct weights.  Tolerances (per tensor, max|gpu-ref| / max|ref| vs the f64
-oracle): FP32_SIMT and TF32X3 1e-5; TF32 (single pass, 10-bit mantissa) 5e-3.
+oracle): FP32_SIMT and TF32X3 1e-5; TF32 (single pass, 10-bit mantissa) 5e-3;
+BF16 (operands rounded to 8-bit significands) 2e-2 -- and, exactly, BF16 equals
+an f64 GEMM of bf16-rounded operands to fp32 accumulation error
+(test_bf16_mode_is_a_bf16_gemm).
 """
 import ctypes as C
 
@@ -13,7 +16,7 @@ from parity import (conv_w_from_dev, conv_w_to_dev, convT_w_from_dev, convT_w_to
 
 pytestmark = pytest.mark.gpu
 
-MODES = [(0, 1e-5), (1, 1e-5), (2, 5e-3)]
+MODES = [(0, 1e-5), (1, 1e-5), (2, 5e-3), (3, 2e-2)]  # BF16: operands rounded to 8-bit significands
 
 
 @pytest.fixture(scope="module")
@@ -499,3 +502,53 @@ def test_image_side_many_labels_per_cta(native, torch_cuda, math, tol):
         worst[name] = float(err)
     assert max(worst.values()) < tol, worst
     assert torch.all(gx_d[..., 3] == 0) and torch.all(yt_d[..., 3] == 0)
+
+
+def bf16_round(a):
+    """numpy restatement of the device's nearest-even bfloat16 rounding (fp32 container)."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
+@pytest.mark.parametrize("case", [(4, 64, 16, 16, 128, 4, 2, 1), (4, 3, 64, 64, 64, 4, 2, 1), (2, 128, 8, 8, 256, 4, 2, 1)])
+def test_bf16_mode_is_a_bf16_gemm(native, torch_cuda, case):
+    """PG_MATH_BF16 on every conv GEMM form (forward, data and weight gradient;
+    pair engine and the 4-channel image-side kernels) equals a float64
+    convolution of the bf16-rounded operands up to fp32 accumulation error:
+    the mode rounds both tensor-core operands and nothing else."""
+    torch = torch_cuda
+    import torch.nn.functional as F
+    from paper_2102_10485_b200 import _native as N
+    B, Cin, H, W, Cout, k, s, p = case
+    L = 2
+    OH, OW = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    rng = np.random.default_rng(5)
+    x = rng.normal(0, 1, (L, B, Cin, H, W)).astype(np.float32)
+    w = rng.normal(0, 0.2, (L, Cout, Cin, k, k)).astype(np.float32)
+    gy = rng.normal(0, 1, (L, B, Cout, OH, OW)).astype(np.float32)
+    xr, wr, gyr = (torch.from_numpy(bf16_round(a)).double() for a in (x, w, gy))
+    y_ref = torch.stack([F.conv2d(xr[l], wr[l], stride=s, padding=p) for l in range(L)])
+    gx_ref = torch.stack([F.conv_transpose2d(gyr[l], wr[l], stride=s, padding=p) for l in range(L)])
+    gw_ref = torch.stack([torch.nn.grad.conv2d_weight(xr[l], wr[l].shape, gyr[l], stride=s, padding=p)
+                          for l in range(L)])
+    wdev = np.stack([conv_w_to_dev(w[l], Cout, Cin, k).ravel() for l in range(L)])
+    x_d = dev(torch, np.stack([nchw_to_nhwc(x[l]) for l in range(L)]))
+    gy_d = dev(torch, np.stack([nchw_to_nhwc(gy[l]) for l in range(L)]))
+    w_d = dev(torch, wdev)
+    b_d = torch.zeros((L, pad4(Cout)), device="cuda")
+    y_d = torch.zeros((L, B, OH, OW, pad4(Cout)), device="cuda")
+    gx_d = torch.zeros((L, B, H, W, pad4(Cin)), device="cuda")
+    gw_d = torch.zeros_like(w_d)
+    d = N.ConvDesc(B=B, Cin=Cin, H=H, W=W, Cout=Cout, OH=OH, OW=OW, k=k, s=s, p=p)
+    N.check(native.pg_conv2d_fwd(C.byref(d), L, ptr(x_d), ptr(w_d), wdev.shape[1], ptr(b_d), pad4(Cout), 0, 0.0,
+                                 ptr(y_d), N.MATH_BF16, None), "fwd")
+    N.check(native.pg_conv2d_bwd_data(C.byref(d), L, ptr(gy_d), ptr(w_d), wdev.shape[1], ptr(gx_d), N.MATH_BF16,
+                                      None), "dgrad")
+    N.check(native.pg_conv2d_bwd_filter(C.byref(d), L, ptr(x_d), ptr(gy_d), ptr(gw_d), wdev.shape[1], 0,
+                                        N.MATH_BF16, None), "wgrad")
+    y, gx, gw = host(y_d), host(gx_d), host(gw_d)
+    for l in range(L):
+        assert rel_max(nhwc_to_nchw(y[l], Cout), y_ref[l].numpy()) < 1e-5
+        assert rel_max(nhwc_to_nchw(gx[l], Cin), gx_ref[l].numpy()) < 1e-5
+        assert rel_max(conv_w_from_dev(gw[l], Cout, Cin, k), gw_ref[l].numpy()) < 1e-5

@@ -635,3 +635,24 @@ def test_cli_config_and_bench(tmp_path):
     lines = (tmp_path / "b" / "scaling.csv").read_text().splitlines()
     assert lines[0] == "k,wall_clock_s,max_worker_s,cores_used,oversubscribed"
     assert [ln.split(",")[0] for ln in lines[1:]] == ["1", "3"]
+
+
+def test_bf16_step_tracks_the_f64_reference(oracle):
+    """PG_MATH_BF16 (GEMM operands rounded to bfloat16, fp32 accumulation and
+    everything else fp32): a c1 step's losses and means stay within 2e-2 of
+    the f64 oracle, a 10-step trajectory within 1e-1 (the GAN dynamics amplify
+    the ~4e-3 per-product rounding), and nothing goes non-finite."""
+    from paper_2102_10485_b200 import _native as N
+    arch, grp = make_pair(1, 2, 640, 64, N.MATH_BF16)
+    orc = oracle.OracleGroup(64, 1, 2, 640, 64, data_seed=3, base_seed=7)
+    assert grp.train_steps(10) == 10
+    orc.step(10)
+    assert not grp.failed().any()
+    for l in range(2):
+        r = grp.reports(l)
+        q = orc.get(l, OR["reports"]).reshape(-1, 4)
+        assert np.isfinite(r).all()
+        rel = np.abs(r - q) / np.abs(q)
+        print(f"label {l}: bf16-vs-f64 step 1 {np.array2string(rel[0], precision=1)}, worst {rel.max():.2e}")
+        assert rel[0].max() < 2e-2, rel[0]
+        assert rel.max() < 1e-1, rel
