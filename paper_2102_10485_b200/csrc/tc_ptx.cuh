@@ -10,15 +10,22 @@
 namespace pg {
 
 // PG_MATH_BF16 operand rounding: nearest-even to bfloat16 (8-bit significand),
-// kept in an fp32 container; inf / NaN pass through.  bf16 values are exact in
+// kept in an fp32 container (the hardware conversion: inf / NaN preserved).  bf16 values are exact in
 // tf32 and their products exact in fp32, so a kind::tf32 MMA on rounded
 // operands is a bf16 x bf16 -> fp32 product.
 PG_DEV float bf16_rne(float x) {
-  const uint32_t u = __float_as_uint(x);
-  if ((u & 0x7F800000u) == 0x7F800000u) return x;
-  return __uint_as_float((u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u);
+  uint16_t h;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(x));
+  return __uint_as_float((uint32_t)h << 16);
 }
-PG_DEV float4 bf16_rne4(float4 v) { return make_float4(bf16_rne(v.x), bf16_rne(v.y), bf16_rne(v.z), bf16_rne(v.w)); }
+// two elements per cvt (one instruction + two to unpack)
+PG_DEV float4 bf16_rne4(float4 v) {
+  uint32_t p0, p1;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p0) : "f"(v.y), "f"(v.x));  // upper half <- first source
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p1) : "f"(v.w), "f"(v.z));
+  return make_float4(__uint_as_float(p0 << 16), __uint_as_float(p0 & 0xFFFF0000u), __uint_as_float(p1 << 16),
+                     __uint_as_float(p1 & 0xFFFF0000u));
+}
 PG_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 PG_DEV void mbar_init(uint64_t* bar, uint32_t count) {
