@@ -245,7 +245,13 @@ GemmWorkspace gemm_workspace(const GemmArgs& a, int math) {
 
 cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
   scratch_call_begin(st);
-  if (a.stat_mode != STAT_NONE && gemm_stat_slots(a, math) == 0) return cudaErrorInvalidValue;
+  if (a.kind == GEMM_WGRAD) {
+    // a weight gradient takes fused statistics only as wgrad4's activation backward
+    if (a.stat_mode != STAT_NONE && (a.stat_mode != STAT_BWD_ACT || !wgrad4_supported(a, math)))
+      return cudaErrorInvalidValue;
+  } else if (a.stat_mode != STAT_NONE && gemm_stat_slots(a, math) == 0) {
+    return cudaErrorInvalidValue;
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {
     cudaEventCreate(&e0);

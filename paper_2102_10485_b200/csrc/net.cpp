@@ -456,6 +456,15 @@ ConvGeo DevNet::geo_for(const Block& b, int B) const {
 // act/BN sums (default off: the y / z reads in the epilogue stall the MMA
 // pipeline more than the separate reduce pass costs, +2.7 ms/step).
 // PG_FUSE overrides the bit set (A/B timing).
+// PG_WG_ACT=0: the discriminator conv1's activation backward as its own pass (A/B timing)
+static bool wg_act_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PG_WG_ACT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool fuse_enabled(int bit) {
   static const int on = [] {
     const char* e = std::getenv("PG_FUSE");
@@ -570,6 +579,23 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
     const float* gz = gy;
     float* dbias = param_grads ? grads.p + b.off_b : nullptr;
     bool bias_done = false;
+    // a conv layer with an activation, no BatchNorm and no input gradient to
+    // produce (the discriminator's conv1 in its own update): its weight-gradient
+    // kernel applies the activation backward to gy on the fly and sums the bias
+    // gradient, so the act_bwd + bias-sum pass over (gy, y) and the g1 map drop out
+    bool wg_act = param_grads && !fused && !b.has_bn && b.act != ACT_NONE && b.lin == LK::Conv && i == 0 && !gx_ext &&
+                  wg_act_enabled();
+    if (wg_act) {  // only the tcgen05 4-channel weight gradient (wgrad4.cu) fuses it
+      GemmArgs probe{};
+      probe.kind = GEMM_WGRAD;
+      probe.g = geo_for(b, B);
+      probe.L = L_;
+      probe.small = gy;
+      probe.small_ls = out_ls;
+      probe.big = t.act[static_cast<size_t>(i)];
+      probe.big_ls = in_ls;
+      wg_act = wgrad4_supported(probe, math_);
+    }
     if (b.has_bn) {
       // bn_bwd_apply takes the activation mask from (pre-BN map, BN coefficients), not the stored y
       static const bool yfree = [] {
@@ -605,6 +631,8 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
                                      b.slope, gz_.p, st, bnc),
                  "bn bwd apply");
       gz = gz_.p;
+    } else if (wg_act) {
+      bias_done = true;  // both come out of the weight-gradient launch below
     } else if (b.act != ACT_NONE && !fused) {
       if (param_grads) {
         // activation backward and the bias sums in one pass over (gy, y)
@@ -669,6 +697,13 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
       a.out = grads.p + b.off_w;
       a.out_ls = P_;
       a.accumulate = accumulate ? 1 : 0;
+      if (wg_act) {
+        a.stat_mode = STAT_BWD_ACT;
+        a.stat_y = t.act[static_cast<size_t>(i) + 1];
+        a.stat_act = b.act;
+        a.stat_slope = b.slope;
+        a.stat = dbias;  // [L] x C bias gradient, label stride P_ (= out_ls)
+      }
       check_cuda(launch_gemm(a, math_, st), "wgrad");
     }
     // 3) input gradient

@@ -380,6 +380,15 @@ __global__ void thin_in_wgrad_reduce_kernel(GemmArgs a, const float* part, int n
   const int l = blockIdx.y;
   const int NN = g.k * g.k * 4;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;  // over CS x NN
+  if (a.stat_mode == STAT_BWD_ACT && e < g.CS && a.stat) {
+    // fused activation backward (wgrad4): the bias gradient from the per-chunk,
+    // per-group channel sums, added in a fixed order
+    const float* bp = part + (size_t)a.L * nchunk * 64 * 64 + (size_t)l * nchunk * 2 * 64 + e;
+    float sb = 0.f;
+    for (int c = 0; c < nchunk; ++c) sb += bp[c * 128] + bp[c * 128 + 64];
+    float* ob = a.stat + l * a.out_ls + e;
+    *ob = a.accumulate ? *ob + sb : sb;
+  }
   if (e >= g.CS * NN) return;
   const int m = e / NN, n = e % NN;
   float s = 0.f;
@@ -547,7 +556,7 @@ bool gemm_thin_supported(const GemmArgs& a) { return classify(a) != T_NONE; }
 size_t gemm_thin_workspace_floats(const GemmArgs& a) {
   if (classify(a) != T_IN_WGRAD) return 0;
   const long long K = (long long)a.g.B * a.g.SH * a.g.SW;
-  return (size_t)a.L * ((K + TW_SPLIT - 1) / TW_SPLIT) * 64 * 64;
+  return (size_t)a.L * ((K + TW_SPLIT - 1) / TW_SPLIT) * 64 * (64 + 2);
 }
 
 cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math) {
@@ -586,7 +595,7 @@ cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math) {
     case T_IN_WGRAD: {
       const long long K = (long long)g.B * g.SH * g.SW;
       const int nchunk = (int)((K + TW_SPLIT - 1) / TW_SPLIT);
-      float* part = gemm_scratch((size_t)a.L * nchunk * 64 * 64, st);
+      float* part = gemm_scratch((size_t)a.L * nchunk * 64 * (64 + 2), st);  // weight + bias partials
       if (!part) return cudaErrorMemoryAllocation;
       cudaError_t e;
       if (wgrad4_supported(a, math)) {

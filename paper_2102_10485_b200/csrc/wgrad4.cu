@@ -44,9 +44,15 @@ namespace {
 
 using namespace tmac;
 
-constexpr int W4_T = 6;          // TMA ring: gy tile + x patch (DRAM latency in flight)
+// Ring depths are multiples of the consumer groups (4 gather groups, 2 A-warp
+// groups): every slot is then always filled / read by the same group, in order.
+// Otherwise a group running ahead can wait on a slot's mbarrier two phases
+// ahead and pass on the older phase of the same parity (a 6-deep operand ring
+// with 4 groups corrupted the c4 weight gradient of some labels).
+constexpr int W4_T = 4;          // TMA ring: gy tile (+ y tile) + x patch
 constexpr int W4_O = 8;          // operand ring: B hi, B lo (gather -> MMA)
 constexpr int W4_AS = 4;         // TMEM A ring: gy^T hi / lo (A warps -> MMA)
+static_assert(W4_T % 4 == 0 && W4_O % 4 == 0 && W4_AS % 2 == 0, "ring depths vs consumer groups");
 constexpr int W4_KB = 32;        // pixels per k-block
 constexpr int W4_KSEG = 8;       // k-blocks per TMEM accumulation segment
 constexpr int W4_CHUNK = 1024;   // pixels per work item (thin.cu TW_SPLIT: same partial layout)
@@ -55,7 +61,7 @@ constexpr int W4_NT = 16 * 32;
 constexpr int W4_A = 64 * 32 * 4;  // gy tile: 32 pixel rows x 64 channels (plain, 256 B rows)
 constexpr int W4_B = 16 * 512;     // B operand: 64 rows (tap, channel) x 32 pixels, K-major SW128
 constexpr int W4_PATCH = 4096;     // input rows of a k-block (patch mode)
-constexpr int W4_TS = W4_A + W4_PATCH;  // TMA slot: gy tile | x patch
+constexpr int W4_TS = 2 * W4_A + W4_PATCH;  // TMA slot: gy tile | y tile (fused activation backward) | x patch
 constexpr int W4_OS = 2 * W4_B;         // operand slot: B lo | B hi
 constexpr int W4_SMEM = W4_T * W4_TS + W4_O * W4_OS + 1024 + 1024;
 constexpr uint32_t W4_ACOL = W4_AS * 64;  // accumulators after the A ring: 2 segments x W4_NACC x 64 columns
@@ -71,6 +77,12 @@ struct W4Plan {
   long long big_ls;
   float* part;
   int patch_rows, patch_bytes;  // patch mode: input rows per k-block, TMA bytes of the patch box
+  // fused activation backward (the small operand is gy of the layer's output,
+  // y its activation output: the GEMM uses act_bwd(gy, y), and the A warps
+  // sum it per channel into bias partials [L][nchunk][2][64])
+  int fuse_act;
+  float slope;
+  float* bpart;
 };
 
 PG_DEV int chunk_kblocks(const W4Plan& P, int chunk) {
@@ -93,6 +105,7 @@ PG_DEV void mma_tf32_ts_w4(uint32_t tmem_d, uint32_t a_tmem, uint64_t bdesc, uin
 // two warps, k-block it % 4 each).
 template <int MODE, bool PATCH>
 __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                         const __grid_constant__ CUtensorMap tmY,
                                                          const __grid_constant__ CUtensorMap tmX, const W4Plan P) {
   constexpr bool X3 = MODE == MATH_TF32X3, RND = MODE == MATH_BF16;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -148,19 +161,21 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
     // ===================== TMA: gy tile (+ x patch) per k-block =====================
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
+      if (P.fuse_act) tma_prefetch_desc(&tmY);
       if (PATCH) tma_prefetch_desc(&tmX);
       uint32_t it = 0;
       for (Cur c = start_at(blockIdx.x); c.t < nitems; adv(c), ++it) {
         const int l = c.t / P.nchunk, chunk = c.t % P.nchunk;
         const int s = it % W4_T;
         mbar_wait(tfree + s, ((it / W4_T) & 1) ^ 1);
-        mbar_expect_tx(full + s, W4_A + (PATCH ? P.patch_bytes : 0));
+        mbar_expect_tx(full + s, W4_A * (P.fuse_act ? 2 : 1) + (PATCH ? P.patch_bytes : 0));
         const int p0 = chunk * W4_CHUNK + c.kb * W4_KB;
         const uint32_t dst = smem_u32(smem + s * W4_TS);
         tma_load_3d(dst, &tmA, full + s, 0, p0, l);
+        if (P.fuse_act) tma_load_3d(dst + W4_A, &tmY, full + s, 0, p0, l);
         if (PATCH) {  // the input rows under the k-block's 32 / SW output rows of image b
           const int r = p0 / g.SW;
-          tma_load_4d(dst + W4_A, &tmX, full + s, 0, (r % g.SH) * g.s - g.p, r / g.SH, l);
+          tma_load_4d(dst + 2 * W4_A, &tmX, full + s, 0, (r % g.SH) * g.s - g.p, r / g.SH, l);
         }
       }
     }
@@ -169,21 +184,39 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
     const int q = warp & 3, par = warp >= 8 ? 1 : 0;
     const int cs = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    float bsum = 0.f;  // fused mode: this group's sum of act_bwd(gy, y) for channel cs over the chunk
     uint32_t it = 0;
+    // each group writes its chunk partial when the loop passes the chunk's last
+    // k-block, whichever group owns it (a one-k-block chunk gives the other 0)
+    auto flush = [&](const Cur& c) {
+      if (P.fuse_act && c.kb + 1 == c.nkb) {
+        P.bpart[(((long long)(c.t / P.nchunk) * P.nchunk + c.t % P.nchunk) * 2 + par) * 64 + cs] = bsum;
+        bsum = 0.f;
+      }
+    };
     for (Cur c = start_at(blockIdx.x); c.t < nitems; adv(c), ++it) {
-      if ((int)(it & 1) != par) continue;
+      if ((int)(it & 1) != par) {
+        flush(c);
+        continue;
+      }
       const int s = it % W4_T, as = it % W4_AS;
       mbar_wait(full + s, (it / W4_T) & 1);
       const float* ga = reinterpret_cast<const float*>(smem + s * W4_TS);
+      const float* ya = ga + W4_A / 4;
       uint32_t hi[32], lo[32];
 #pragma unroll
       for (int px = 0; px < 32; ++px) {
-        const float v = ga[px * 64 + cs];  // a warp reads one 128-byte run per pixel row
+        float v = ga[px * 64 + cs];  // a warp reads one 128-byte run per pixel row
+        if (P.fuse_act) {
+          v = act_bwd(P.fuse_act, v, ya[px * 64 + cs], P.slope);
+          bsum += v;  // pixels past K are zero-filled by TMA
+        }
         hi[px] = __float_as_uint(RND ? bf16_rne(v) : v);
         lo[px] = __float_as_uint(v - tf32_trunc(v));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(tfree + s);
+      flush(c);
       mbar_wait(afree + as, ((it / W4_AS) & 1) ^ 1);
       tc_fence_after();
       tmem_st32(tmem + lane_off + as * 64, hi);
@@ -238,7 +271,7 @@ __global__ void __launch_bounds__(W4_NT, 1) wgrad4_kernel(const __grid_constant_
       }
       mbar_wait(full + s, (it / W4_T) & 1);          // gy (+ patch) landed
       if (PATCH) {
-        const float4* xp = reinterpret_cast<const float4*>(smem + s * W4_TS + W4_A);
+        const float4* xp = reinterpret_cast<const float4*>(smem + s * W4_TS + 2 * W4_A);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           int tap, px;
@@ -382,12 +415,20 @@ cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, 
   P.big = a.big;
   P.big_ls = a.big_ls;
   P.part = part;
-  CUtensorMap tm;
+  // STAT_BWD_ACT on a weight gradient: `small` is the raw output gradient, stat_y
+  // the activation output (same layout); the bias partials follow the weight partials
+  P.fuse_act = a.stat_mode == STAT_BWD_ACT ? a.stat_act : 0;
+  P.slope = a.stat_slope;
+  P.bpart = part + (size_t)a.L * nchunk * 64 * 64;
+  CUtensorMap tm, ty;
   const long long dims[3] = {g.CS, P.K, a.L};
   const long long strides[2] = {g.CS, a.small_ls};
   const int box[3] = {64, W4_KB, 1};
   const int one[3] = {1, 1, 1};
   if (!make_map(&tm, a.small, 3, dims, strides, box, one, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  ty = tm;
+  if (P.fuse_act && !make_map(&ty, a.stat_y, 3, dims, strides, box, one, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   // patch mode: a k-block = 32 / SW whole output rows of one image, whose input
   // rows (GW * 4 floats each) arrive as one TMA box next to the gy boxes
@@ -416,8 +457,8 @@ cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, 
   const int items = a.L * nchunk;
   const int grid = std::min(items, sm_count_tma());
 #define PG_W4(M)                                                            \
-  (patch ? wgrad4_kernel<M, true><<<grid, W4_NT, W4_SMEM, st>>>(tm, tx, P)  \
-         : wgrad4_kernel<M, false><<<grid, W4_NT, W4_SMEM, st>>>(tm, tx, P))
+  (patch ? wgrad4_kernel<M, true><<<grid, W4_NT, W4_SMEM, st>>>(tm, ty, tx, P)  \
+         : wgrad4_kernel<M, false><<<grid, W4_NT, W4_SMEM, st>>>(tm, ty, tx, P))
   if (math == MATH_TF32X3) PG_W4(MATH_TF32X3);
   else if (math == MATH_BF16) PG_W4(MATH_BF16);
   else PG_W4(MATH_TF32);
