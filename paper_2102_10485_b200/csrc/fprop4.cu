@@ -28,7 +28,6 @@
 #include <cuda.h>
 #include <stdint.h>
 
-#include <cstdio>
 #include <cstdlib>
 
 #include "device_cache.hpp"
@@ -414,15 +413,7 @@ cudaError_t launch_fprop4(const GemmArgs& a, int math, cudaStream_t st) {
     fprop4_kernel<MATH_BF16><<<grid, F4_NT, F4_SMEM, st>>>(tx, tw, to, P);
   else
     fprop4_kernel<MATH_TF32><<<grid, F4_NT, F4_SMEM, st>>>(tx, tw, to, P);
-  const cudaError_t le = launched();
-  if (le != cudaSuccess && std::getenv("PG_F4_DIAG")) {
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, fprop4_kernel<MATH_TF32X3>);
-    fprintf(stderr, "fprop4 launch: %s regs=%d maxthreads=%d smem_static=%zu maxdyn=%d local=%zu want dyn=%d threads=%d\n",
-            cudaGetErrorString(le), fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes,
-            fa.localSizeBytes, F4_SMEM, F4_NT);
-  }
-  return le;
+  return launched();
 }
 
 }  // namespace pg
