@@ -219,7 +219,7 @@ enum class Mode { train, eval };
 
 // Device-side options of a network / pair (not in the reference API).
 struct DeviceOptions {
-  int math = PG_MATH_TF32X3;
+  int math = PG_MATH_TF32X3;  // PG_MATH_{FP32_SIMT, TF32X3 (fp32-accurate), TF32, BF16} (pg_kernels.h)
   int device = 0;
 };
 
