@@ -399,16 +399,20 @@ __global__ void thin_in_wgrad_reduce_kernel(GemmArgs a, const float* part, int n
 
 // ---- dense heads ----------------------------------------------------------
 // FPROP with N = CS <= 4: out[b][0:CS] = x[b] . W[0:CS] (warp per (label, b))
-__global__ void dense_fprop_n4_kernel(GemmArgs a) {
+// FPROP with N = CS <= 4 (the discriminator head, K = 6272 / 4096 / 8192):
+// block = (row b, label), each thread's float4s of the row loaded at once (a
+// warp per row left ~8% of the loads in flight that HBM latency needs), then
+// a fixed-order block reduction (lane tree, then the eight warps in order)
+constexpr int DN4_NT = 256;
+__global__ void __launch_bounds__(DN4_NT) dense_fprop_n4_kernel(GemmArgs a) {
   const ConvGeo& g = a.g;
-  const int l = blockIdx.y;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
-  if (warp >= g.B) return;
-  const float* x = a.big + l * a.big_ls + (long long)warp * g.CG;
+  const int l = blockIdx.y, b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const float* x = a.big + l * a.big_ls + (long long)b * g.CG;
   const float* w = a.w + l * a.w_ls;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-  for (int k = lane * 4; k < g.CG; k += 128) {  // unrolled: loads of 4 iterations in flight, same sum order
+#pragma unroll 8
+  for (int k = tid * 4; k < g.CG; k += DN4_NT * 4) {
     const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
 #pragma unroll
     for (int n = 0; n < 4; ++n)
@@ -417,13 +421,18 @@ __global__ void dense_fprop_n4_kernel(GemmArgs a) {
         acc[n] = fmaf(xv.x, wv.x, fmaf(xv.y, wv.y, fmaf(xv.z, wv.z, fmaf(xv.w, wv.w, acc[n]))));
       }
   }
+  __shared__ float part[DN4_NT / 32][4];
 #pragma unroll
-  for (int n = 0; n < 4; ++n)
+  for (int n = 0; n < 4; ++n) {
     for (int o = 16; o > 0; o >>= 1) acc[n] += __shfl_xor_sync(0xffffffffu, acc[n], o);
-  if (lane == 0) {
-    float* out = a.out + l * a.out_ls + (long long)warp * g.CS;
+    if (lane == 0) part[warp][n] = acc[n];
+  }
+  __syncthreads();
+  if (tid < g.CS) {
+    float s = 0.f;
+    for (int wi = 0; wi < DN4_NT / 32; ++wi) s += part[wi][tid];
     const float* bias = a.bias ? a.bias + l * a.bias_ls : nullptr;
-    for (int n = 0; n < g.CS; ++n) out[n] = epi(a, bias, n, acc[n]);
+    a.out[l * a.out_ls + (long long)b * g.CS + tid] = epi(a, bias, tid, s);
   }
 }
 
@@ -460,32 +469,35 @@ __global__ void __launch_bounds__(128) dense_fprop_smallk_kernel(GemmArgs a) {
     if (b < B) out[(long long)b * g.CS] = epi(a, bias, n, acc[b]);
 }
 
-// DGRAD with K = CS <= 4: gx[b][f] = sum_cs gz[b][cs] W[cs][f]
-__global__ void __launch_bounds__(256) dense_dgrad_k4_kernel(GemmArgs a) {
-  // grid-stride over the float4s of [B][CG/4]: the output write is the whole
-  // cost, so each thread streams several float4 (one per block was
-  // block-scheduling bound at ~1.7 TB/s)
+// DGRAD with K = CS <= 4: gx[b][f] = sum_cs gz[b][cs] W[cs][f]; block =
+// (row b, label), every thread's float4s issued together (32-bit indexing: the
+// grid-stride form spent its time in 64-bit divisions and one store in flight)
+__global__ void __launch_bounds__(DN4_NT) dense_dgrad_k4_kernel(GemmArgs a) {
   const ConvGeo& g = a.g;
-  const int l = blockIdx.y;
-  const int f4n = g.CG / 4;
-  const long long n = (long long)g.B * f4n;
+  const int l = blockIdx.y, b = blockIdx.x;
   const float* w = a.w + l * a.w_ls;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
-    const int b = (int)(q / f4n), f = (int)(q % f4n) * 4;
-    const float* gz = a.small + l * a.small_ls + (long long)b * g.CS;
+  const float* gz = a.small + l * a.small_ls + (long long)b * g.CS;
+  float gv[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) gv[c] = c < g.CS ? __ldg(gz + c) : 0.f;
+  float* out = a.out + l * a.out_ls + (long long)b * g.CG;
+#pragma unroll 8
+  for (int f = threadIdx.x * 4; f < g.CG; f += DN4_NT * 4) {
     float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c = 0; c < g.CS; ++c) {
-      const float gv = gz[c];
-      const float4 wv = __ldg(reinterpret_cast<const float4*>(w + (long long)c * g.CG + f));
-      r.x = fmaf(gv, wv.x, r.x);
-      r.y = fmaf(gv, wv.y, r.y);
-      r.z = fmaf(gv, wv.z, r.z);
-      r.w = fmaf(gv, wv.w, r.w);
-    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < g.CS) {
+        const float4 wv = __ldg(reinterpret_cast<const float4*>(w + c * g.CG + f));
+        r.x = fmaf(gv[c], wv.x, r.x);
+        r.y = fmaf(gv[c], wv.y, r.y);
+        r.z = fmaf(gv[c], wv.z, r.z);
+        r.w = fmaf(gv[c], wv.w, r.w);
+      }
     float o[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
     for (int u = 0; u < 4; ++u)
       if ((f + u) % a.c_pad >= a.c_valid) o[u] = 0.f;
-    *reinterpret_cast<float4*>(a.out + l * a.out_ls + (long long)b * g.CG + f) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(out + f) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -615,19 +627,16 @@ cudaError_t launch_gemm_thin(const GemmArgs& a, cudaStream_t st, int math) {
       break;
     }
     case T_D_FPROP_N4:
-      dense_fprop_n4_kernel<<<dim3((unsigned)((g.B * 32 + 255) / 256), a.L), 256, 0, st>>>(a);
+      dense_fprop_n4_kernel<<<dim3((unsigned)g.B, a.L), DN4_NT, 0, st>>>(a);
       break;
     case T_D_FPROP_SK: {
       const size_t smem = (size_t)g.B * g.CG * sizeof(float);
       dense_fprop_smallk_kernel<<<dim3((unsigned)((g.CS + 127) / 128), a.L), 128, smem, st>>>(a);
       break;
     }
-    case T_D_DGRAD_K4: {
-      const long long n = (long long)g.B * (g.CG / 4);
-      const long long per_block = 256 * 8;  // eight float4 per thread
-      dense_dgrad_k4_kernel<<<dim3((unsigned)((n + per_block - 1) / per_block), a.L), 256, 0, st>>>(a);
+    case T_D_DGRAD_K4:
+      dense_dgrad_k4_kernel<<<dim3((unsigned)g.B, a.L), DN4_NT, 0, st>>>(a);
       break;
-    }
     case T_D_WGRAD_M4:
       dense_wgrad_m4_kernel<<<dim3((unsigned)((g.CG / 4 + 255) / 256), a.L), 256, 0, st>>>(a);
       break;
