@@ -92,6 +92,15 @@ struct GemmArgs {
   const float* stat_mu;  // BWD_BN: batch mean [L][N]
   int stat_act;
   float stat_slope;
+  // activation backward applied to the small operand as it is loaded (the
+  // 4-channel image-side kernels only: wgrad4.cu, dgrad4.cu): the GEMM uses
+  // act_bwd(small, in_y) with in_y the layer's activation output (same layout
+  // and label stride as small); WGRAD also writes the bias gradient
+  // sum_rows act_bwd(...) to in_dbias ([L] x CS, label stride out_ls)
+  int in_act;  // ACT_NONE: off
+  float in_slope;
+  const float* in_y;
+  float* in_dbias;
 };
 
 // phase decomposition of the big map along one axis for stride s, pad p:

@@ -245,13 +245,10 @@ GemmWorkspace gemm_workspace(const GemmArgs& a, int math) {
 
 cudaError_t launch_gemm(const GemmArgs& a, int math, cudaStream_t st) {
   scratch_call_begin(st);
-  if (a.kind == GEMM_WGRAD) {
-    // a weight gradient takes fused statistics only as wgrad4's activation backward
-    if (a.stat_mode != STAT_NONE && (a.stat_mode != STAT_BWD_ACT || !wgrad4_supported(a, math)))
-      return cudaErrorInvalidValue;
-  } else if (a.stat_mode != STAT_NONE && gemm_stat_slots(a, math) == 0) {
+  if (a.stat_mode != STAT_NONE && (a.kind == GEMM_WGRAD || gemm_stat_slots(a, math) == 0)) return cudaErrorInvalidValue;
+  // the input-side activation backward exists only in the 4-channel image-side kernels
+  if (a.in_act != ACT_NONE && !(a.kind == GEMM_WGRAD ? wgrad4_supported(a, math) : dgrad4_supported(a, math)))
     return cudaErrorInvalidValue;
-  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {
     cudaEventCreate(&e0);

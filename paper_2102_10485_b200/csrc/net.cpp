@@ -698,11 +698,10 @@ void DevNet::backward(Trace& t, int B, const float* gy_ext, bool param_grads, bo
       a.out_ls = P_;
       a.accumulate = accumulate ? 1 : 0;
       if (wg_act) {
-        a.stat_mode = STAT_BWD_ACT;
-        a.stat_y = t.act[static_cast<size_t>(i) + 1];
-        a.stat_act = b.act;
-        a.stat_slope = b.slope;
-        a.stat = dbias;  // [L] x C bias gradient, label stride P_ (= out_ls)
+        a.in_act = b.act;
+        a.in_slope = b.slope;
+        a.in_y = t.act[static_cast<size_t>(i) + 1];
+        a.in_dbias = dbias;  // [L] x C bias gradient, label stride P_ (= out_ls)
       }
       check_cuda(launch_gemm(a, math_, st), "wgrad");
     }

@@ -380,13 +380,13 @@ __global__ void thin_in_wgrad_reduce_kernel(GemmArgs a, const float* part, int n
   const int l = blockIdx.y;
   const int NN = g.k * g.k * 4;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;  // over CS x NN
-  if (a.stat_mode == STAT_BWD_ACT && e < g.CS && a.stat) {
+  if (a.in_act != ACT_NONE && e < g.CS && a.in_dbias) {
     // fused activation backward (wgrad4): the bias gradient from the per-chunk,
     // per-group channel sums, added in a fixed order
     const float* bp = part + (size_t)a.L * nchunk * 64 * 64 + (size_t)l * nchunk * 2 * 64 + e;
     float sb = 0.f;
     for (int c = 0; c < nchunk; ++c) sb += bp[c * 128] + bp[c * 128 + 64];
-    float* ob = a.stat + l * a.out_ls + e;
+    float* ob = a.in_dbias + l * a.out_ls + e;
     *ob = a.accumulate ? *ob + sb : sb;
   }
   if (e >= g.CS * NN) return;

@@ -415,10 +415,10 @@ cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, 
   P.big = a.big;
   P.big_ls = a.big_ls;
   P.part = part;
-  // STAT_BWD_ACT on a weight gradient: `small` is the raw output gradient, stat_y
-  // the activation output (same layout); the bias partials follow the weight partials
-  P.fuse_act = a.stat_mode == STAT_BWD_ACT ? a.stat_act : 0;
-  P.slope = a.stat_slope;
+  // input-side activation backward (GemmArgs::in_act): `small` is the raw output
+  // gradient, in_y the activation output; the bias partials follow the weight partials
+  P.fuse_act = a.in_act;
+  P.slope = a.in_slope;
   P.bpart = part + (size_t)a.L * nchunk * 64 * 64;
   CUtensorMap tm, ty;
   const long long dims[3] = {g.CS, P.K, a.L};
@@ -428,7 +428,7 @@ cudaError_t launch_wgrad4(const GemmArgs& a, int math, float* part, int nchunk, 
   if (!make_map(&tm, a.small, 3, dims, strides, box, one, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   ty = tm;
-  if (P.fuse_act && !make_map(&ty, a.stat_y, 3, dims, strides, box, one, CU_TENSOR_MAP_SWIZZLE_NONE))
+  if (P.fuse_act && !make_map(&ty, a.in_y, 3, dims, strides, box, one, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   // patch mode: a k-block = 32 / SW whole output rows of one image, whose input
   // rows (GW * 4 floats each) arrive as one TMA box next to the gy boxes
