@@ -68,7 +68,7 @@ def build(verbose: bool = False) -> Path:
                     print("built", obj.name)
     objs = [OBJ / (s.name + ".o") for s in srcs]
     if not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        cmd = [NVCC, *ARCH, *CCBIN, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs), "-lpthread"]
+        cmd = [NVCC, *ARCH, *CCBIN, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs), "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -154,19 +154,25 @@ PG_DEV float sum_partials(const ChannelMap& cm, const float* partial, int l, int
 // reference K (the first entry's shift, a value of the channel itself) and
 // summed in f64: with d' = shift - K,  S1 += sum_d + n d',  S2 += sum_d2 +
 // 2 d' sum_d + n d'^2  -- additions only (the per-slot Chan merge spent most of
-// the kernel in f64 divisions).  Block = 32 channels x nl lanes: lane j sums
-// the (slot, pack column) entries j, j + nl, ... in order, then a fixed
-// pairwise tree adds the lanes (deterministic, independent of timing).
+// the kernel in f64 divisions).  Block = FIN_CW channels x nl lanes (thread
+// t: channel t % FIN_CW, lane t / FIN_CW, so a warp reads four 32-byte entry
+// rows): lane j sums the (slot, pack column) entries j, j + nl, ... in order,
+// then a fixed pairwise tree adds the lanes (deterministic, independent of
+// timing).  Eight channels per block (not 32) give 4x the blocks and 4x the
+// lanes per channel, so a launch is one short wave instead of ~2 waves of
+// 11-deep serial load -> f64 chains (16 -> 73 us on the 1376-slot c4 maps).
 struct Sums {
   double n, s1, s2;
 };
-constexpr int FIN_MAX_LANES = 32;
-__global__ void __launch_bounds__(32 * FIN_MAX_LANES) bn_stats_finalize_kernel(ChannelMap cm, const float* stat,
-                                                                              float* mean, float* istd, float* running,
-                                                                              long long run_ls, float eps, float mom,
-                                                                              int update) {
-  const int l = blockIdx.y, c = blockIdx.x * 32 + threadIdx.x, j = threadIdx.y, nl = blockDim.y;
-  __shared__ Sums sm[FIN_MAX_LANES][32];
+constexpr int FIN_CW = 8;          // channels per block
+constexpr int FIN_MAX_LANES = 128;  // lanes per channel
+__global__ void __launch_bounds__(FIN_CW * FIN_MAX_LANES) bn_stats_finalize_kernel(ChannelMap cm, const float* stat,
+                                                                                  float* mean, float* istd,
+                                                                                  float* running, long long run_ls,
+                                                                                  float eps, float mom, int update) {
+  const int cl = threadIdx.x % FIN_CW, j = threadIdx.x / FIN_CW, nl = blockDim.x / FIN_CW;
+  const int l = blockIdx.y, c = blockIdx.x * FIN_CW + cl;
+  __shared__ Sums sm[FIN_MAX_LANES][FIN_CW];
   Sums a{0.0, 0.0, 0.0};
   const int W = cm.Cp * cm.npack;  // statistic row width
   const float* base = stat + (long long)l * cm.nslot * 4 * W + (c < cm.Cp ? c : 0);
@@ -198,15 +204,15 @@ __global__ void __launch_bounds__(32 * FIN_MAX_LANES) bn_stats_finalize_kernel(C
       }
     }
   }
-  sm[j][threadIdx.x] = a;
+  sm[j][cl] = a;
   for (int h = nl / 2; h > 0; h >>= 1) {
     __syncthreads();
     if (j < h) {
-      const Sums b = sm[j + h][threadIdx.x];
+      const Sums b = sm[j + h][cl];
       a.n += b.n;
       a.s1 += b.s1;
       a.s2 += b.s2;
-      sm[j][threadIdx.x] = a;
+      sm[j][cl] = a;
     }
   }
   if (j != 0 || c >= cm.Cp) return;
@@ -779,7 +785,7 @@ cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* m
 
 // lanes per channel: about 8 entries per lane, 4..32 (few entries: small blocks)
 static int fin_lanes(const ChannelMap& cm) {
-  int nl = 4;
+  int nl = 32;  // >= 256 threads per block
   while (nl < FIN_MAX_LANES && nl * 8 < cm.nslot * cm.npack) nl <<= 1;
   return nl;
 }
@@ -787,10 +793,12 @@ static int fin_lanes(const ChannelMap& cm) {
 cudaError_t launch_bn_stats_finalize(const ChannelMap& cm, const float* stat, float* mean, float* istd, float* running,
                                      long long run_ls, float eps, float momentum, int update_running, cudaStream_t st) {
   if (cm.nslot <= 0) return cudaErrorInvalidValue;
-  bn_stats_finalize_kernel<<<dim3((cm.Cp + 31) / 32, cm.L), dim3(32, fin_lanes(cm)), 0, st>>>(cm, stat, mean, istd, running,
-                                                                                  run_ls, eps, momentum,
-                                                                                  update_running);
-  return launched();
+  cudaEvent_t t0_ = timing_start(st);
+  bn_stats_finalize_kernel<<<dim3((cm.Cp + FIN_CW - 1) / FIN_CW, cm.L), FIN_CW * fin_lanes(cm), 0, st>>>(
+      cm, stat, mean, istd, running, run_ls, eps, momentum, update_running);
+  cudaError_t r_ = launched();
+  timing_stop(t0_, st, "hbm bn_stats_finalize bytes=" + std::to_string(16LL * cm.L * cm.nslot * cm.Cp * cm.npack));
+  return r_;
 }
 
 cudaError_t launch_slot_sum(const ChannelMap& cm, const float* stat, float* out, cudaStream_t st) {
