@@ -154,25 +154,19 @@ PG_DEV float sum_partials(const ChannelMap& cm, const float* partial, int l, int
 // reference K (the first entry's shift, a value of the channel itself) and
 // summed in f64: with d' = shift - K,  S1 += sum_d + n d',  S2 += sum_d2 +
 // 2 d' sum_d + n d'^2  -- additions only (the per-slot Chan merge spent most of
-// the kernel in f64 divisions).  Block = FIN_CW channels x nl lanes (thread
-// t: channel t % FIN_CW, lane t / FIN_CW, so a warp reads four 32-byte entry
-// rows): lane j sums the (slot, pack column) entries j, j + nl, ... in order,
-// then a fixed pairwise tree adds the lanes (deterministic, independent of
-// timing).  Eight channels per block (not 32) give 4x the blocks and 4x the
-// lanes per channel, so a launch is one short wave instead of ~2 waves of
-// 11-deep serial load -> f64 chains (16 -> 73 us on the 1376-slot c4 maps).
+// the kernel in f64 divisions).  Block = 32 channels x nl lanes: lane j sums
+// the (slot, pack column) entries j, j + nl, ... in order, then a fixed
+// pairwise tree adds the lanes (deterministic, independent of timing).
 struct Sums {
   double n, s1, s2;
 };
-constexpr int FIN_CW = 8;          // channels per block
-constexpr int FIN_MAX_LANES = 128;  // lanes per channel
-__global__ void __launch_bounds__(FIN_CW * FIN_MAX_LANES) bn_stats_finalize_kernel(ChannelMap cm, const float* stat,
-                                                                                  float* mean, float* istd,
-                                                                                  float* running, long long run_ls,
-                                                                                  float eps, float mom, int update) {
-  const int cl = threadIdx.x % FIN_CW, j = threadIdx.x / FIN_CW, nl = blockDim.x / FIN_CW;
-  const int l = blockIdx.y, c = blockIdx.x * FIN_CW + cl;
-  __shared__ Sums sm[FIN_MAX_LANES][FIN_CW];
+constexpr int FIN_MAX_LANES = 32;
+__global__ void __launch_bounds__(32 * FIN_MAX_LANES) bn_stats_finalize_kernel(ChannelMap cm, const float* stat,
+                                                                              float* mean, float* istd, float* running,
+                                                                              long long run_ls, float eps, float mom,
+                                                                              int update) {
+  const int l = blockIdx.y, c = blockIdx.x * 32 + threadIdx.x, j = threadIdx.y, nl = blockDim.y;
+  __shared__ Sums sm[FIN_MAX_LANES][32];
   Sums a{0.0, 0.0, 0.0};
   const int W = cm.Cp * cm.npack;  // statistic row width
   const float* base = stat + (long long)l * cm.nslot * 4 * W + (c < cm.Cp ? c : 0);
@@ -204,15 +198,15 @@ __global__ void __launch_bounds__(FIN_CW * FIN_MAX_LANES) bn_stats_finalize_kern
       }
     }
   }
-  sm[j][cl] = a;
+  sm[j][threadIdx.x] = a;
   for (int h = nl / 2; h > 0; h >>= 1) {
     __syncthreads();
     if (j < h) {
-      const Sums b = sm[j + h][cl];
+      const Sums b = sm[j + h][threadIdx.x];
       a.n += b.n;
       a.s1 += b.s1;
       a.s2 += b.s2;
-      sm[j][cl] = a;
+      sm[j][threadIdx.x] = a;
     }
   }
   if (j != 0 || c >= cm.Cp) return;
@@ -648,10 +642,13 @@ __global__ void gather_real_kernel(int B, const int* __restrict__ idx, const flo
   const int l = blockIdx.z, b = blockIdx.y;
   const long long src = (long long)l * data_ls + (long long)idx[l * B + b] * sample;
   const long long dst = ((long long)l * B + b) * sample;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < sample / 4;
-       q += (long long)gridDim.x * blockDim.x) {
-    float4 v = reinterpret_cast<const float4*>(data + src)[q];
-    int c0 = (int)((q * 4) % Cp);
+  // 32-bit index arithmetic (a sample is < 2^31 floats; the 64-bit modulo was
+  // a software division per float4)
+  const int n4 = (int)(sample / 4);
+#pragma unroll 4
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += gridDim.x * blockDim.x) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(data + src) + q);
+    int c0 = (4 * q) % Cp;
     float r[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int u = 0; u < 4; ++u) r[u] = (c0 + u < C) ? r[u] * 2.f - 1.f : 0.f;
@@ -785,7 +782,7 @@ cudaError_t launch_bn_apply(const ChannelMap& cm, const float* x, const float* m
 
 // lanes per channel: about 8 entries per lane, 4..32 (few entries: small blocks)
 static int fin_lanes(const ChannelMap& cm) {
-  int nl = 32;  // >= 256 threads per block
+  int nl = 4;
   while (nl < FIN_MAX_LANES && nl * 8 < cm.nslot * cm.npack) nl <<= 1;
   return nl;
 }
@@ -794,8 +791,9 @@ cudaError_t launch_bn_stats_finalize(const ChannelMap& cm, const float* stat, fl
                                      long long run_ls, float eps, float momentum, int update_running, cudaStream_t st) {
   if (cm.nslot <= 0) return cudaErrorInvalidValue;
   cudaEvent_t t0_ = timing_start(st);
-  bn_stats_finalize_kernel<<<dim3((cm.Cp + FIN_CW - 1) / FIN_CW, cm.L), FIN_CW * fin_lanes(cm), 0, st>>>(
-      cm, stat, mean, istd, running, run_ls, eps, momentum, update_running);
+  bn_stats_finalize_kernel<<<dim3((cm.Cp + 31) / 32, cm.L), dim3(32, fin_lanes(cm)), 0, st>>>(cm, stat, mean, istd, running,
+                                                                                  run_ls, eps, momentum,
+                                                                                  update_running);
   cudaError_t r_ = launched();
   timing_stop(t0_, st, "hbm bn_stats_finalize bytes=" + std::to_string(16LL * cm.L * cm.nslot * cm.Cp * cm.npack));
   return r_;
@@ -903,7 +901,7 @@ cudaError_t launch_adam(int L, long long P, float* params, const float* grads, f
 cudaError_t launch_gather_real(int L, int B, const int* idx, const float* data, long long data_ls, long long sample,
                                int Cp, int C, float* out, cudaStream_t st) {
   cudaEvent_t t0_ = timing_start(st);
-  dim3 grid(grid_for(sample / 4, 256, 16), B, L);
+  dim3 grid(grid_for(sample / 4, 256 * 4, 16), B, L);  // ~4 float4 per thread
   gather_real_kernel<<<grid, 256, 0, st>>>(B, idx, data, data_ls, sample, Cp, C, out);
   cudaError_t r_ = launched();
   timing_stop(t0_, st, "hbm gather_real bytes=" + std::to_string((long long)(8LL * L * B * sample)));

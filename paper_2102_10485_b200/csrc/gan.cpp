@@ -13,7 +13,7 @@ namespace pg {
 
 namespace {
 // NVTX range over the host enqueue of one phase of the step: a profiler can
-// select a phase's kernels with it (ncu --nvtx --nvtx-include "pg/D update/"),
+// select a phase's kernels with it (ncu --nvtx --nvtx-include "pg.D_update/"),
 // a no-op when no tool is attached
 struct Phase {
   explicit Phase(const char* name) { nvtxRangePushA(name); }
@@ -293,7 +293,7 @@ void GanGroup::enqueue_step_kernels(int B, const float* real_nhwc, int par, cuda
   // per-launch timing (bench.py's roofline pass) serialises the step: events
   // around a launch would otherwise also time whatever the other stream runs
   const bool ov = overlap_ && !gemm_timing_on();
-  const Phase step_range("pg/step");
+  const Phase step_range("pg.step");
   cudaStream_t gs = ov ? st2_ : st_;
   Trace& tg2 = ov ? tg2_ : tg_;
   if (ov) {
@@ -301,7 +301,7 @@ void GanGroup::enqueue_step_kernels(int B, const float* real_nhwc, int par, cuda
     check_cuda(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork wait");
   }
   // discriminator update on (real, fresh fake); the generator trace is dropped
-  std::optional<Phase> phase(std::in_place, "pg/G forward");
+  std::optional<Phase> phase(std::in_place, "pg.G_forward");
   tg_.act[0] = dz_[par][0].p;
   G_->forward(tg_, B, true, true, gs);
   if (capture_) capture_pass(*G_, tg_, B, 0, gs);
@@ -313,7 +313,7 @@ void GanGroup::enqueue_step_kernels(int B, const float* real_nhwc, int par, cuda
     if (capture_) capture_pass(*G_, tg2, B, gsz + 2 * dsz, st2_);
     check_cuda(cudaEventRecord(ev_g2_, st2_), "g2");
   }
-  phase.emplace("pg/D update");
+  phase.emplace("pg.D_update");
   tdr_.act[0] = const_cast<float*>(real_nhwc);
   if (real_ready) check_cuda(cudaStreamWaitEvent(st_, real_ready, 0), "wait real batch");
   D_->forward(tdr_, B, true, true, st_);
@@ -334,7 +334,7 @@ void GanGroup::enqueue_step_kernels(int B, const float* real_nhwc, int par, cuda
                          static_cast<float>(cfg_.eps), st_),
              "adam D");
   // generator update through the updated discriminator (its grads discarded)
-  phase.emplace("pg/G update");
+  phase.emplace("pg.G_update");
   if (ov) {
     check_cuda(cudaStreamWaitEvent(st_, ev_g2_, 0), "join g2");
   } else {
