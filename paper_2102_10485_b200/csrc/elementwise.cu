@@ -161,6 +161,7 @@ struct Sums {
   double n, s1, s2;
 };
 constexpr int FIN_MAX_LANES = 32;
+template <bool PACK1>  // npack == 1: entry k at 4 W k (no integer division per entry)
 __global__ void __launch_bounds__(32 * FIN_MAX_LANES) bn_stats_finalize_kernel(ChannelMap cm, const float* stat,
                                                                               float* mean, float* istd, float* running,
                                                                               long long run_ls, float eps, float mom,
@@ -180,7 +181,8 @@ __global__ void __launch_bounds__(32 * FIN_MAX_LANES) bn_stats_finalize_kernel(C
         const int k = k0 + u * nl;
         e0[u] = e1[u] = e2[u] = e3[u] = 0.f;
         if (k < items) {
-          const float* e = base + (long long)(k / cm.npack) * 4 * W + (k % cm.npack) * cm.Cp;
+          const float* e = PACK1 ? base + (long long)k * 4 * W
+                                 : base + (long long)(k / cm.npack) * 4 * W + (k % cm.npack) * cm.Cp;
           e0[u] = e[0];
           e1[u] = e[W];
           e2[u] = e[2 * W];
@@ -791,9 +793,13 @@ cudaError_t launch_bn_stats_finalize(const ChannelMap& cm, const float* stat, fl
                                      long long run_ls, float eps, float momentum, int update_running, cudaStream_t st) {
   if (cm.nslot <= 0) return cudaErrorInvalidValue;
   cudaEvent_t t0_ = timing_start(st);
-  bn_stats_finalize_kernel<<<dim3((cm.Cp + 31) / 32, cm.L), dim3(32, fin_lanes(cm)), 0, st>>>(cm, stat, mean, istd, running,
-                                                                                  run_ls, eps, momentum,
-                                                                                  update_running);
+  const dim3 grid((cm.Cp + 31) / 32, cm.L), block(32, fin_lanes(cm));
+  if (cm.npack == 1)
+    bn_stats_finalize_kernel<true><<<grid, block, 0, st>>>(cm, stat, mean, istd, running, run_ls, eps, momentum,
+                                                           update_running);
+  else
+    bn_stats_finalize_kernel<false><<<grid, block, 0, st>>>(cm, stat, mean, istd, running, run_ls, eps, momentum,
+                                                            update_running);
   cudaError_t r_ = launched();
   timing_stop(t0_, st, "hbm bn_stats_finalize bytes=" + std::to_string(16LL * cm.L * cm.nslot * cm.Cp * cm.npack));
   return r_;
