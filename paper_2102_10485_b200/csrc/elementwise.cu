@@ -148,6 +148,40 @@ PG_DEV float sum_partials(const ChannelMap& cm, const float* partial, int l, int
   return t;
 }
 
+// The three sums k = 0, 1, 2 of sum_partials at once: 24 loads in flight
+// instead of 8, each sum added in chunk order (bit-identical to three calls)
+PG_DEV void sum_partials3(const ChannelMap& cm, const float* partial, int l, int c, float& t0, float& t1,
+                          float& t2) {
+  const int nchunk = cm.nslot > 0 ? cm.nslot : (cm.R + red_rows(cm) - 1) / red_rows(cm);
+  const int pk = cm.nslot > 0 ? 4 : 3;
+  const float* p = partial + (long long)l * nchunk * pk * cm.Cp + c;
+  const long long step = (long long)pk * cm.Cp;
+  t0 = t1 = t2 = 0.f;
+  int ch = 0;
+  for (; ch + 8 <= nchunk; ch += 8) {
+    float v0[8], v1[8], v2[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float* q = p + (ch + u) * step;
+      v0[u] = __ldg(q);
+      v1[u] = __ldg(q + cm.Cp);
+      v2[u] = __ldg(q + 2 * cm.Cp);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      t0 += v0[u];
+      t1 += v1[u];
+      t2 += v2[u];
+    }
+  }
+  for (; ch < nchunk; ++ch) {
+    const float* q = p + ch * step;
+    t0 += __ldg(q);
+    t1 += __ldg(q + cm.Cp);
+    t2 += __ldg(q + 2 * cm.Cp);
+  }
+}
+
 // Per-slot {shift, sum d, sum d^2, n} (d = z - shift) -> mean and biased
 // variance over all rows (network.cpp:171-184), running stats as
 // bn_finalize_var.  The slots are re-expressed against one per-channel
@@ -371,9 +405,8 @@ __global__ void bn_bwd_finalize_kernel(ChannelMap cm, const float* partial, cons
     return;
   }
   const float m = (float)cm.R;
-  const float S1 = sum_partials(cm, partial, l, 0, c);
-  const float S2 = sum_partials(cm, partial, l, 1, c);
-  const float S3 = sum_partials(cm, partial, l, 2, c);
+  float S1, S2, S3;
+  sum_partials3(cm, partial, l, c, S1, S2, S3);
   const float is = istd[i];
   const float gamma = gb[(long long)l * gb_ls + c];
   float dg = S2 * is, db = S1;
