@@ -131,18 +131,18 @@ __global__ void __launch_bounds__(RED_NT) channel_reduce_kernel(ChannelMap cm, c
 PG_DEV float sum_partials(const ChannelMap& cm, const float* partial, int l, int k, int c) {
   const int nchunk = cm.nslot > 0 ? cm.nslot : (cm.R + red_rows(cm) - 1) / red_rows(cm);
   const int pk = cm.nslot > 0 ? 4 : 3;
-  // eight loads in flight, added in chunk order (the sum is bit-identical to
+  // sixteen loads in flight, added in chunk order (the sum is bit-identical to
   // the plain loop; the plain loop waited one load latency per chunk)
   const float* p = partial + ((long long)l * nchunk * pk + k) * cm.Cp + c;
   const long long step = (long long)pk * cm.Cp;
   float t = 0.f;
   int ch = 0;
-  for (; ch + 8 <= nchunk; ch += 8) {
-    float v[8];
+  for (; ch + 16 <= nchunk; ch += 16) {
+    float v[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (ch + u) * step);
+    for (int u = 0; u < 16; ++u) v[u] = __ldg(p + (ch + u) * step);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t += v[u];
+    for (int u = 0; u < 16; ++u) t += v[u];
   }
   for (; ch < nchunk; ++ch) t += __ldg(p + ch * step);
   return t;
@@ -195,7 +195,7 @@ struct Sums {
   double n, s1, s2;
 };
 constexpr int FIN_MAX_LANES = 32;
-template <bool PACK1>  // npack == 1: entry k at 4 W k (no integer division per entry)
+template <int NP>  // npack when 1 or 4 (shift / mask instead of an integer division per entry), 0: runtime
 __global__ void __launch_bounds__(32 * FIN_MAX_LANES) bn_stats_finalize_kernel(ChannelMap cm, const float* stat,
                                                                               float* mean, float* istd, float* running,
                                                                               long long run_ls, float eps, float mom,
@@ -215,8 +215,8 @@ __global__ void __launch_bounds__(32 * FIN_MAX_LANES) bn_stats_finalize_kernel(C
         const int k = k0 + u * nl;
         e0[u] = e1[u] = e2[u] = e3[u] = 0.f;
         if (k < items) {
-          const float* e = PACK1 ? base + (long long)k * 4 * W
-                                 : base + (long long)(k / cm.npack) * 4 * W + (k % cm.npack) * cm.Cp;
+          const int np = NP ? NP : cm.npack;
+          const float* e = base + (long long)(k / np) * 4 * W + (k % np) * cm.Cp;
           e0[u] = e[0];
           e1[u] = e[W];
           e2[u] = e[2 * W];
@@ -828,11 +828,14 @@ cudaError_t launch_bn_stats_finalize(const ChannelMap& cm, const float* stat, fl
   cudaEvent_t t0_ = timing_start(st);
   const dim3 grid((cm.Cp + 31) / 32, cm.L), block(32, fin_lanes(cm));
   if (cm.npack == 1)
-    bn_stats_finalize_kernel<true><<<grid, block, 0, st>>>(cm, stat, mean, istd, running, run_ls, eps, momentum,
-                                                           update_running);
+    bn_stats_finalize_kernel<1><<<grid, block, 0, st>>>(cm, stat, mean, istd, running, run_ls, eps, momentum,
+                                                        update_running);
+  else if (cm.npack == 4)
+    bn_stats_finalize_kernel<4><<<grid, block, 0, st>>>(cm, stat, mean, istd, running, run_ls, eps, momentum,
+                                                        update_running);
   else
-    bn_stats_finalize_kernel<false><<<grid, block, 0, st>>>(cm, stat, mean, istd, running, run_ls, eps, momentum,
-                                                            update_running);
+    bn_stats_finalize_kernel<0><<<grid, block, 0, st>>>(cm, stat, mean, istd, running, run_ls, eps, momentum,
+                                                        update_running);
   cudaError_t r_ = launched();
   timing_stop(t0_, st, "hbm bn_stats_finalize bytes=" + std::to_string(16LL * cm.L * cm.nslot * cm.Cp * cm.npack));
   return r_;
